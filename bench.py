@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the B200 RGB-D segmentation path.
+
+Metric (BASELINE.json): "Mpixel/s and fps at 1920x1080 RGB-D (GMM, PBAS),
+1/2/4/8 B200, % HBM roofline".
+
+Default workload = BASELINE config 4 at its per-GPU share: 8 independent
+1920x1080 RGB-D camera streams per GPU (64 on 8 GPUs), every frame segmented
+by BOTH the GMM (paper default k_rgb=7, k_d=3) and PBAS (n=20).
+One step = one frame of every stream of this rank through both algorithms:
+one batched GMM launch + one batched PBAS classify launch + one batched PBAS
+apply launch.  `value` = whole-job Mpixel/s (pixels of all streams of all
+ranks per second, each pixel segmented by both algorithms); weak scaling
+(per-GPU work fixed as N grows).
+
+Inputs: SURVEY.md §8(d) regimes, generated untimed and uploaded to HBM as a
+frame ring per stream: GMM runs on regime S (every component seeded, so the
+algorithmic byte count is honest), PBAS on regime T (moving objects + depth
+holes).  The state is burned in to steady state before the warm-up steps
+(GMM: all 7/3 components seeded; PBAS: 2n = 40 frames, dmin rings full).
+The per-step working set (5.8 GB GMM + 2.5 GB PBAS state per GPU) is far
+larger than L2, so no explicit flush is needed.
+
+Extra keys: roofline (GMM K1, the dominant kernel), per-algorithm breakdown,
+cpu_baseline (the oracle port on this host's cores), e2e (the public
+SegmentationEngine host-buffer path with H2D/D2H inside the timed region),
+clocks (nvidia-smi sampled during the timed region), gpu_launches.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port of the numba kernels, oracle/, all host threads) on the same
+workload, one 1080p stream-frame (GMM + PBAS) per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2002_00250_b200 import synth  # noqa: E402
+from paper_2002_00250_b200.config import GmmParams, PbasParams, PipelineConfig  # noqa: E402
+
+METRIC = "Mpixel/s and fps at 1920x1080 RGB-D (GMM, PBAS), 1/2/4/8 B200, % HBM roofline"
+UNIT = "Mpixel/s"
+# SURVEY.md §8(d) algorithmic bytes per pixel per frame (B_alg).
+B_ALG = {("gmm", 7, 3): 485, ("gmm", 3, 3): 293, ("pbas", 20): 181}
+
+WORKLOADS = {
+    # name: (width, height, streams per GPU, gmm (k_rgb, k_d) or None, pbas n or None)
+    "config4": (1920, 1080, 8, (7, 3), 20),
+    "config3": (1280, 720, 1, (7, 3), 20),
+    "config1": (640, 480, 1, (3, 3), None),
+    "config2": (640, 480, 1, None, 20),
+}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = [ln.split(",") for ln in Path(self.f.name).read_text().splitlines() if ln.strip()]
+        os.unlink(self.f.name)
+        sms, maxes, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            try:
+                sms.append(float(r[1]))
+                maxes.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(maxes),
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# --------------------------------------------------------------- frames ---
+def _gen_ring(regime, w, h, seeds, ring, k_rgb=7):
+    jobs = [(s, t) for s in seeds for t in range(ring)]
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        frames = list(ex.map(lambda st: synth.make_frame(regime, w, h, st[0], st[1], k_rgb), jobs))
+    return np.stack(frames).reshape(len(seeds), ring, h, w, 4)
+
+
+# --------------------------------------------------------- CPU baseline ----
+def cpu_sample(w, h, gmm_k, pbas_n, seed, budget_s=12.0, max_frames=12, workers=None):
+    """Time the oracle port (reference algorithm, CPU) on a bounded sample:
+    one w x h stream, GMM + PBAS per frame, after an untimed burn-in."""
+    from oracle import oracle
+
+    oracle.build()
+    workers = workers or oracle.cpu_threads()
+    engines = []
+    if gmm_k:
+        g = oracle.OracleEngine(PipelineConfig(algorithm="gmm", mode="rgbd",
+                                               gmm=GmmParams(k_rgb=gmm_k[0], k_d=gmm_k[1])),
+                                w, h, workers=workers)
+        engines.append((g, "S", 8))
+    if pbas_n:
+        p = oracle.OracleEngine(PipelineConfig(algorithm="pbas", mode="rgbd",
+                                               pbas=PbasParams(n=pbas_n), seed=seed + 1),
+                                w, h, workers=workers)
+        engines.append((p, "T", pbas_n + 2))
+    ring = {r: [synth.make_frame(r, w, h, seed, t, gmm_k[0] if gmm_k else 7) for t in range(7)]
+            for r in {e[1] for e in engines}}
+    for eng, reg, burn in engines:
+        for t in range(burn):
+            eng.process_frame(ring[reg][t % 7])
+    frames, elapsed = 0, 0.0
+    while frames < max_frames and (elapsed < budget_s or frames < 2):
+        t0 = time.perf_counter()
+        for eng, reg, _ in engines:
+            eng.process_frame(ring[reg][frames % 7])
+        elapsed += time.perf_counter() - t0
+        frames += 1
+    return {"value": w * h * frames / elapsed / 1e6, "unit": UNIT, "cores": workers,
+            "kind": "port", "frames": frames, "seconds": elapsed,
+            "sample": f"{frames} frames of one {w}x{h} stream through "
+                      f"{'GMM %d/%d' % gmm_k if gmm_k else ''}"
+                      f"{' + ' if gmm_k and pbas_n else ''}{'PBAS n=%d' % pbas_n if pbas_n else ''}"
+                      f" (oracle/ C port of the numba kernels, {workers} threads, after burn-in)"}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    w, h, _, gmm_k, pbas_n = WORKLOADS[args.workload]
+    from oracle import oracle
+
+    oracle.build()
+    workers = oracle.cpu_threads()
+    engines = []
+    if gmm_k:
+        engines.append((oracle.OracleEngine(
+            PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=gmm_k[0], k_d=gmm_k[1])),
+            w, h, workers=workers), "S", 8))
+    if pbas_n:
+        engines.append((oracle.OracleEngine(
+            PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=pbas_n), seed=1),
+            w, h, workers=workers), "T", pbas_n + 2))
+    ring = {r: [synth.make_frame(r, w, h, 0, t, gmm_k[0] if gmm_k else 7) for t in range(7)]
+            for r in {e[1] for e in engines}}
+    for eng, reg, burn in engines:
+        for t in range(burn):
+            eng.process_frame(ring[reg][t % 7])
+
+    def step(i):
+        for eng, reg, _ in engines:
+            eng.process_frame(ring[reg][i % 7])
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    value = w * h * args.steps / dt / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64/u8", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: reference CPU path, one {w}x{h} RGB-D stream-frame "
+                               f"per step", "width": w, "height": h,
+                   "gmm": list(gmm_k) if gmm_k else None, "pbas_n": pbas_n},
+        "fps": args.steps / dt,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"{args.steps} timed steps x one {w}x{h} frame (GMM+PBAS), "
+                                   f"oracle/ C port of the reference numba kernels, {workers} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- GPU arm ---
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_00250_b200.engine import MultiStreamEngine
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w, h, S, gmm_k, pbas_n = WORKLOADS[args.workload]
+    if args.streams:
+        S = args.streams
+    npix = w * h
+    stream_ids = [rank * S + i for i in range(S)]  # global stream ids (content seeds)
+
+    # ---- engines + device frame rings (untimed setup)
+    algos = []
+    if gmm_k:
+        gcfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=gmm_k[0], k_d=gmm_k[1]))
+        g = MultiStreamEngine(gcfg, w, h, S, device=local_rank, seeds=[s + 1 for s in stream_ids])
+        ring_s = torch.from_numpy(_gen_ring("S", w, h, stream_ids, gmm_k[0], gmm_k[0])).to(dev)
+        algos.append(("gmm", g, ring_s, B_ALG.get(("gmm",) + tuple(gmm_k))))
+    if pbas_n:
+        pcfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=pbas_n))
+        p = MultiStreamEngine(pcfg, w, h, S, device=local_rank, seeds=[s + 1 for s in stream_ids])
+        ring_t = torch.from_numpy(_gen_ring("T", w, h, stream_ids, 8)).to(dev)
+        algos.append(("pbas", p, ring_t, B_ALG.get(("pbas", pbas_n))))
+    masks = torch.empty((S, h, w), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    mbase = masks.data_ptr()
+    mptrs = [mbase + i * npix for i in range(S)]
+
+    def launch(name, eng, ring, t):
+        R = ring.shape[1]
+        base = ring.data_ptr()
+        fptrs = [base + ((i * R) + (t % R)) * npix * 4 for i in range(S)]
+        eng.step_ptrs(fptrs, mptrs, sptr)
+
+    burn = max([8 if a[0] == "gmm" else 2 * pbas_n for a in algos])
+    for t in range(burn):
+        for name, eng, ring, _ in algos:
+            launch(name, eng, ring, t)
+    torch.cuda.synchronize()
+
+    # ---- warm-up + timed region
+    launches_per_step = sum(1 if a[0] == "gmm" else 2 for a in algos)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(algos) + 1)]
+          for _ in range(args.steps)]
+    t_frame = burn
+    for _ in range(args.warmup):
+        for name, eng, ring, _ in algos:
+            launch(name, eng, ring, t_frame)
+        t_frame += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(int(os.environ.get("RGBDSEG_NVSMI_INDEX", local_rank)))
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        for j, (name, eng, ring, _) in enumerate(algos):
+            launch(name, eng, ring, t_frame)
+            ev[k][j + 1].record(stream)
+        t_frame += 1
+    end.record(stream)
+    torch.cuda.synchronize()
+    clock_info = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = start.elapsed_time(end)
+    per_algo_ms = {a[0]: [ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)]
+                   for j, a in enumerate(algos)}
+
+    # ---- final metric reduction (NCCL all-reduce of counters, once per run)
+    fg = torch.count_nonzero(masks).to(torch.int64)
+    counters = torch.stack([fg, torch.tensor(masks.numel(), device=dev, dtype=torch.int64)])
+    t_max = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
+    elapsed_ms = float(t_max.item())
+    ms_step = elapsed_ms / args.steps
+    total_px = npix * S * world * args.steps
+    value = total_px / (elapsed_ms / 1e3) / 1e6
+    fps = S * world * args.steps / (elapsed_ms / 1e3)
+
+    peak, peak_kind = measured_peaks()
+    per_algo = {}
+    for name, eng, ring, balg in algos:
+        avg_ms = statistics.mean(per_algo_ms[name])
+        mpx = npix * S / (avg_ms / 1e3) / 1e6
+        d = {"ms_per_step": avg_ms, "mpix_s_per_gpu": mpx, "fps_per_stream": 1e3 / avg_ms,
+             "bytes_per_pixel_alg": balg}
+        if balg:
+            gbs = balg * npix * S / (avg_ms / 1e3) / 1e9
+            d.update({"achieved_gbs": gbs, "roofline_frac": gbs / peak})
+        per_algo[name] = d
+    dom = "gmm" if "gmm" in per_algo else "pbas"
+    traffic = None
+    tfile = ROOT / "profiles" / "traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(f"{dom}:{args.workload}")
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": per_algo[dom].get("achieved_gbs"), "peak": peak,
+            "unit": "GB/s", "frac": per_algo[dom].get("roofline_frac"), "traffic": traffic,
+            "kernel": "gmm_step_kernel<7,3> (K1)" if dom == "gmm" else "pbas_classify_kernel (K2)",
+            "peak_kind": peak_kind,
+            "bytes_per_launch_alg": (per_algo[dom]["bytes_per_pixel_alg"] or 0) * npix * S}
+
+    # ---- e2e through the public host-buffer API (rank-local, then max)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, algos, S, w, h, dev, world)
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_sample(w, h, gmm_k, pbas_n, seed=0, budget_s=args.cpu_budget)
+        except Exception as exc:  # report, never fail the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        wl_desc = (f"{args.workload}: {S} x {w}x{h} RGB-D streams per GPU"
+                   + (f", GMM {gmm_k[0]}/{gmm_k[1]} (regime S)" if gmm_k else "")
+                   + (f", PBAS n={pbas_n} (regime T)" if pbas_n else ""))
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64/u8",
+            "data": "synthetic (SURVEY.md §8(d) regimes S/T, seeded per stream)",
+            "config": {"workload": wl_desc, "width": w, "height": h, "streams_per_gpu": S,
+                       "streams_total": S * world,
+                       "gmm": list(gmm_k) if gmm_k else None, "pbas_n": pbas_n,
+                       "burn_in_frames": burn,
+                       "l2": "inputs larger than L2 (state per step "
+                             f"{sum((a[3] or 0) for a in algos) * npix * S / 1e9:.1f} GB >> 126 MB)",
+                       "parallelism": f"streams sharded {S}/GPU over {world} GPU(s)"},
+            "fps": fps,
+            "per_algo": per_algo,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clock_info,
+            "fg_fraction_last_step": float(counters[0].item()) / float(counters[1].item()),
+        }
+        print(json.dumps(line), flush=True)
+    for _, eng, _, _ in algos:
+        eng.close()
+    return 0
+
+
+def run_e2e(args, algos, S, w, h, dev, world):
+    """Same workload through SegmentationEngine.submit (host buffers): per
+    step every stream's frame is copied H2D from pinned memory for each
+    algorithm and the mask read back D2H, all inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    npix = w * h
+    steps = max(3, min(args.steps, args.e2e_steps))
+    host = {}
+    for name, eng, ring, _ in algos:
+        R = ring.shape[1]
+        pinned = torch.empty(ring.shape, dtype=torch.uint8, pin_memory=True)
+        pinned.copy_(ring)
+        outs = torch.empty((S, h, w), dtype=torch.uint8, pin_memory=True)
+        host[name] = (pinned, pinned.numpy(), outs, outs.numpy(), R)
+
+    def step(t):
+        for name, eng, ring, _ in algos:
+            _, fr, _, mk, R = host[name]
+            for i in range(S):
+                eng.engines[i].submit(fr[i, t % R], mk[i])
+        for name, eng, _, _ in algos:
+            for e in eng.engines:
+                e.synchronize()
+
+    for t in range(2):
+        step(t)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for t in range(steps):
+        step(2 + t)
+    dt = time.perf_counter() - t0
+    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    dt = float(tt.item())
+    n_alg = len(algos)
+    return {"value": npix * S * world * steps / dt / 1e6, "unit": UNIT,
+            "h2d_bytes_per_step": 4 * npix * S * n_alg, "d2h_bytes_per_step": npix * S * n_alg,
+            "steps": steps, "timing": "host perf_counter over synchronised steps (spans H2D+D2H)",
+            "api": "SegmentationEngine.submit/synchronize (pinned host buffers, one CUDA stream per engine)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
+    ap.add_argument("--streams", type=int, default=0, help="override streams per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,204 @@
+/*
+ * rgbdseg_b200.h -- C-ABI of the B200-native RGB-D segmentation path.
+ *
+ * Drop-in for the reference's per-pixel segmentation layer
+ * (/root/reference/pkg, citations relative to it).  The reference has no
+ * native FFI of its own (it is Python + numba); the boundary it exposes is
+ *   - the engine: SegmentationEngine.__init__ / process_frame / state_arrays
+ *     (src/rgbdseg/engine.py:60-83, :99-112, :96-97), and
+ *   - the per-algorithm "plugin" calls the engine makes:
+ *     GmmState.segment_rows   (src/rgbdseg/gmm.py:272-280),
+ *     PbasState.segment_rows  (src/rgbdseg/pbas.py:320-333),
+ *     PbasState.apply_intents (src/rgbdseg/pbas.py:335-337),
+ *     GmmState/PbasState.arrays (gmm.py:251-255, pbas.py:296-303).
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain C types only: pointers, sizes, fixed-width integers, doubles.
+ *   - Device memory for the model state is owned by the handle (allocated
+ *     once at create, like GmmState/PbasState).
+ *   - `frame` is packed (H, W, 4) uint8 (r, g, b, d), d == 0 = invalid depth
+ *     (frames.py:46-70); `mask` is (H, W) uint8, 0 = background, 255 =
+ *     foreground.  *_dev pointers are CUDA device pointers; *_host pointers
+ *     are host pointers (pinned memory gives full-speed DMA).
+ *   - `stream` is a cudaStream_t passed as void*; NULL means the handle's own
+ *     stream.  One frame in flight per handle; handles are not thread-safe
+ *     (the service serialises per session: service.py:416-418).
+ *   - Return codes map onto the reference's exception classes
+ *     (src/rgbdseg/errors.py:4-21):
+ *       RGBDSEG_OK 0, RGBDSEG_E_DIMENSION 1 -> DimensionError,
+ *       RGBDSEG_E_CONFIG 2 -> ConfigError, RGBDSEG_E_RUNTIME 3 -> RgbdSegError
+ *     with a message from rgbdseg_last_error() (thread-local).
+ */
+#ifndef RGBDSEG_B200_H
+#define RGBDSEG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RGBDSEG_OK 0
+#define RGBDSEG_E_DIMENSION 1
+#define RGBDSEG_E_CONFIG 2
+#define RGBDSEG_E_RUNTIME 3
+
+#define RGBDSEG_ABI_VERSION 1
+
+/* GmmParams (src/rgbdseg/gmm.py:37-62).  Validation = GmmParams.validate. */
+typedef struct rgbdseg_gmm_params {
+    int32_t k_rgb;
+    int32_t k_d;
+    double alpha;
+    double s;
+    double tau;
+    double match_lambda;
+    double var_init;
+    double w_init;
+} rgbdseg_gmm_params;
+
+/* PbasParams (src/rgbdseg/pbas.py:37-63).  Validation = PbasParams.validate,
+ * plus n <= 255 (u8 pos/len state, pbas.py:288-291). */
+typedef struct rgbdseg_pbas_params {
+    int32_t n;
+    int32_t min_matches;
+    double r_init;
+    double r_lower;
+    double r_scale;
+    double r_inc_dec;
+    double t_init;
+    double t_lower;
+    double t_upper;
+    double t_inc;
+    double t_dec;
+} rgbdseg_pbas_params;
+
+typedef struct rgbdseg_gmm rgbdseg_gmm;   /* opaque */
+typedef struct rgbdseg_pbas rgbdseg_pbas; /* opaque */
+
+/* State field ids; read/write use the reference layout and dtypes. */
+enum {
+    RGBDSEG_GMM_RGB_W = 0,   /* (H,W,k_rgb)   f64   gmm.py:244 */
+    RGBDSEG_GMM_RGB_MU = 1,  /* (H,W,k_rgb,3) f64   gmm.py:245 */
+    RGBDSEG_GMM_RGB_VAR = 2, /* (H,W,k_rgb)   f64   gmm.py:246 */
+    RGBDSEG_GMM_D_W = 3,     /* (H,W,k_d)     f64   gmm.py:247 */
+    RGBDSEG_GMM_D_MU = 4,    /* (H,W,k_d,1)   f64   gmm.py:248 */
+    RGBDSEG_GMM_D_VAR = 5    /* (H,W,k_d)     f64   gmm.py:249 */
+};
+enum {
+    RGBDSEG_PBAS_SAMPLES = 0,  /* (H,W,n,4) u8  pbas.py:285 */
+    RGBDSEG_PBAS_DMIN_RGB = 1, /* (H,W,n)   u8  pbas.py:286 */
+    RGBDSEG_PBAS_DMIN_D = 2,   /* (H,W,n)   u8  pbas.py:287 */
+    RGBDSEG_PBAS_LEN_RGB = 3,  /* (H,W)     u8  pbas.py:288 */
+    RGBDSEG_PBAS_POS_RGB = 4,  /* (H,W)     u8  pbas.py:289 */
+    RGBDSEG_PBAS_LEN_D = 5,    /* (H,W)     u8  pbas.py:290 */
+    RGBDSEG_PBAS_POS_D = 6,    /* (H,W)     u8  pbas.py:291 */
+    RGBDSEG_PBAS_R_RGB = 7,    /* (H,W)     f64 pbas.py:292 */
+    RGBDSEG_PBAS_R_D = 8,      /* (H,W)     f64 pbas.py:293 */
+    RGBDSEG_PBAS_T = 9         /* (H,W)     f64 pbas.py:294 */
+};
+
+/* ------------------------------------------------------------ common ---- */
+const char* rgbdseg_last_error(void);
+int32_t rgbdseg_abi_version(void);
+/* Number of visible CUDA devices (0 when there is no GPU); never fails. */
+int32_t rgbdseg_device_count(void);
+
+/* Device twin of the counter-based RNG, for tests
+ * (engine_rng.pixel_rng / rng_stream, src/rgbdseg/engine_rng.py:55-64):
+ * out_host[i] = pixel_rng(seed, x, y, frame_idx, i) for i < count, computed
+ * by the same __device__ code the PBAS kernel inlines. */
+int rgbdseg_rng_stream(uint64_t seed, uint64_t x, uint64_t y, uint64_t frame_idx, int64_t count,
+                       double* out_host, int32_t device);
+/* Batched draws: out_host[i] = pixel_rng(keys[5i..5i+4]) on the device. */
+int rgbdseg_rng_keys(const uint64_t* keys_host, int64_t count, double* out_host, int32_t device);
+
+/* --------------------------------------------------------------- GMM ---- */
+/* GmmState(width, height, params) (gmm.py:238-249) + engine setup
+ * (engine.py:60-72).  use_depth = (config.mode == "rgbd"). */
+int rgbdseg_gmm_create(int32_t width, int32_t height, const rgbdseg_gmm_params* params,
+                       int32_t use_depth, int32_t device, rgbdseg_gmm** out);
+void rgbdseg_gmm_destroy(rgbdseg_gmm* h);
+
+/* One frame, device buffers: GmmState.segment_rows over all rows
+ * (gmm.py:272-280 -> _gmm_band gmm.py:350-368).  Enqueued on `stream`. */
+int rgbdseg_gmm_step(rgbdseg_gmm* h, const uint8_t* frame_dev, uint8_t* mask_dev, void* stream);
+
+/* Multi-camera batching: one launch advances `count` independent handles
+ * (same k_rgb/k_d/use_depth/device).  The reference has no multi-stream
+ * scheduler; this is the B200 grid over (stream, pixel). */
+int rgbdseg_gmm_step_batch(rgbdseg_gmm* const* hs, int32_t count, const uint8_t* const* frames_dev,
+                           uint8_t* const* masks_dev, void* stream);
+
+/* SegmentationEngine.process_frame with host buffers (engine.py:99-112):
+ * H2D of the frame, the step, D2H of the mask, on the handle's stream.
+ * sync != 0 waits for completion; sync == 0 returns after enqueueing (the
+ * caller must keep both host buffers alive until rgbdseg_gmm_sync). */
+int rgbdseg_gmm_process_host(rgbdseg_gmm* h, const uint8_t* frame_host, uint8_t* mask_host,
+                             int32_t sync);
+int rgbdseg_gmm_sync(rgbdseg_gmm* h);
+
+/* state_arrays()[field] (gmm.py:251-255), reference layout, synchronous. */
+int64_t rgbdseg_gmm_state_bytes(const rgbdseg_gmm* h, int32_t field);
+int rgbdseg_gmm_read_state(rgbdseg_gmm* h, int32_t field, void* host_dst, int64_t bytes);
+int rgbdseg_gmm_write_state(rgbdseg_gmm* h, int32_t field, const void* host_src, int64_t bytes);
+/* The handle's own CUDA stream (cudaStream_t as void*). */
+void* rgbdseg_gmm_stream(rgbdseg_gmm* h);
+
+/* -------------------------------------------------------------- PBAS ---- */
+/* PbasState(width, height, params) (pbas.py:279-294) + engine setup
+ * (engine.py:60-78).  seed = config.seed as u64 (engine.py:127). */
+int rgbdseg_pbas_create(int32_t width, int32_t height, const rgbdseg_pbas_params* params,
+                        int32_t use_depth, uint64_t seed, int32_t device, rgbdseg_pbas** out);
+/* Row band [y0, y1) of a (width x height) frame: the multi-GPU split of one
+ * oversized frame (engine.py:48-50 bands, one per GPU).  RNG keys and
+ * neighbour bounds use GLOBAL coordinates (pbas.py:470-500). */
+int rgbdseg_pbas_create_band(int32_t width, int32_t height, int32_t y0, int32_t y1,
+                             const rgbdseg_pbas_params* params, int32_t use_depth, uint64_t seed,
+                             int32_t device, rgbdseg_pbas** out);
+void rgbdseg_pbas_destroy(rgbdseg_pbas* h);
+
+/* One full frame = classify (PbasState.segment_rows, pbas.py:320-333) +
+ * intent application (PbasState.apply_intents, pbas.py:335-337), then
+ * frame_idx += 1 (engine.py:111).  frame_dev covers the handle's rows. */
+int rgbdseg_pbas_step(rgbdseg_pbas* h, const uint8_t* frame_dev, uint8_t* mask_dev, void* stream);
+/* The two phases separately, for row bands: classify emits this band's
+ * intent codes (own rows + which neighbour + slot); the caller then moves
+ * the edge rows into the neighbours' halos (rgbdseg_pbas_halo_ptrs) and
+ * calls apply, which pulls every intent targeting this band's pixels and
+ * advances frame_idx. */
+int rgbdseg_pbas_classify(rgbdseg_pbas* h, const uint8_t* frame_dev, uint8_t* mask_dev,
+                          void* stream);
+int rgbdseg_pbas_apply(rgbdseg_pbas* h, const uint8_t* frame_dev, void* stream);
+/* Device pointers of the intent rows: the band's first/last own rows and
+ * the halo rows above/below it; each row is row_bytes long.  Halo rows hold
+ * "no intent" unless the caller fills them between classify and apply. */
+int rgbdseg_pbas_halo_ptrs(rgbdseg_pbas* h, void** first_row, void** last_row, void** halo_above,
+                           void** halo_below, int64_t* row_bytes);
+int rgbdseg_pbas_step_batch(rgbdseg_pbas* const* hs, int32_t count,
+                            const uint8_t* const* frames_dev, uint8_t* const* masks_dev,
+                            void* stream);
+int rgbdseg_pbas_process_host(rgbdseg_pbas* h, const uint8_t* frame_host, uint8_t* mask_host,
+                              int32_t sync);
+int rgbdseg_pbas_sync(rgbdseg_pbas* h);
+uint64_t rgbdseg_pbas_get_frame_idx(const rgbdseg_pbas* h);
+int rgbdseg_pbas_set_frame_idx(rgbdseg_pbas* h, uint64_t frame_idx);
+int64_t rgbdseg_pbas_state_bytes(const rgbdseg_pbas* h, int32_t field);
+int rgbdseg_pbas_read_state(rgbdseg_pbas* h, int32_t field, void* host_dst, int64_t bytes);
+int rgbdseg_pbas_write_state(rgbdseg_pbas* h, int32_t field, const void* host_src, int64_t bytes);
+void* rgbdseg_pbas_stream(rgbdseg_pbas* h);
+
+/* ---------------------------------------------------- evaluation ------- */
+/* Confusion counts of a device mask against a device ground-truth label
+ * plane (0 bg / 1 fg / 2 ignore; frames.py:27-29), accumulated into
+ * counts_dev[4] = {tp, tn, fp, fn} (int64): metrics.compare_masks
+ * (src/rgbdseg/metrics.py:50-69) fused on the device. */
+int rgbdseg_confusion_accumulate(const uint8_t* mask_dev, const uint8_t* labels_dev, int64_t npix,
+                                 int64_t* counts_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RGBDSEG_B200_H */

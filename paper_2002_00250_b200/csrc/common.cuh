@@ -1,0 +1,87 @@
+// Shared device/host helpers for the rgbdseg B200 kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/rgbdseg_b200.h"
+
+namespace rgbdseg {
+
+// ------------------------------------------------------------ errors -----
+void set_error(const char* fmt, ...);
+
+#define RGBDSEG_CUDA_TRY(expr)                                                          \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            ::rgbdseg::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,             \
+                                 cudaGetErrorString(_e));                               \
+            return RGBDSEG_E_RUNTIME;                                                   \
+        }                                                                               \
+    } while (0)
+
+#define RGBDSEG_LAUNCH_CHECK()                                                          \
+    do {                                                                                \
+        cudaError_t _e = cudaGetLastError();                                            \
+        if (_e != cudaSuccess) {                                                        \
+            ::rgbdseg::set_error("%s:%d kernel launch: %s", __FILE__, __LINE__,         \
+                                 cudaGetErrorString(_e));                               \
+            return RGBDSEG_E_RUNTIME;                                                   \
+        }                                                                               \
+    } while (0)
+
+// Scoped device switch (restores the caller's current device).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Round a plane length up so every plane of 8/16/32-byte records starts on a
+// 256-byte boundary (full-sector, 256-bit-load friendly).
+inline int64_t plane_pitch(int64_t npix) { return (npix + 31) / 32 * 32; }
+
+// ------------------------------------------------- counter-based RNG -----
+// Device twin of engine_rng.py:15-44 (SplitMix64 finalizer chain).  The
+// (seed, x, y, frame) prefix is shared by the three draws of a pixel
+// (pbas.py:470, :479, :492): 3 + 3 mixes instead of 12.
+constexpr uint64_t RNG_SALT = 0x5851F42D4C957F2DULL;
+constexpr uint64_t RNG_KX = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t RNG_KY = 0xC2B2AE3D27D4EB4FULL;
+constexpr uint64_t RNG_KF = 0x165667B19E3779F9ULL;
+constexpr uint64_t RNG_KD = 0xD6E8FEB86659FD93ULL;
+constexpr uint64_t RNG_M1 = 0xBF58476D1CE4E5B9ULL;
+constexpr uint64_t RNG_M2 = 0x94D049BB133111EBULL;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * RNG_M1;
+    z = (z ^ (z >> 27)) * RNG_M2;
+    return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t rng_prefix(uint64_t seed, uint64_t x, uint64_t y,
+                                                        uint64_t f) {
+    uint64_t h = seed ^ RNG_SALT;
+    h = mix64(h ^ (x * RNG_KX));
+    h = mix64(h ^ (y * RNG_KY));
+    return mix64(h ^ (f * RNG_KF));
+}
+
+__host__ __device__ __forceinline__ double rng_draw(uint64_t prefix, uint64_t d) {
+    uint64_t h = mix64(prefix ^ (d * RNG_KD));
+    return (double)(h >> 11) * (1.0 / 9007199254740992.0);  // exact: (h>>11) < 2^53
+}
+
+}  // namespace rgbdseg

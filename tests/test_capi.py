@@ -1,0 +1,95 @@
+"""CPU-only checks of the C-ABI boundary: the library loads, exports every
+symbol include/rgbdseg_b200.h declares, and maps status codes onto the
+reference's exception classes (errors.py:4-21) -- no compute calls."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2002_00250_b200 import _build, _native
+from paper_2002_00250_b200.config import GmmParams, PbasParams, PipelineConfig
+from paper_2002_00250_b200.errors import ConfigError, DeviceError, DimensionError, RgbdSegError
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "rgbdseg_b200.h"
+
+
+def header_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(rgbdseg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_builds_for_sm100a():
+    lib = _build.build()
+    assert lib.exists()
+
+
+def test_exports_every_declared_symbol():
+    L = _native.lib()
+    declared = header_functions()
+    assert len(declared) >= 30
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(declared) == set(_native.EXPORTS)
+
+
+def test_abi_version_and_device_count():
+    L = _native.lib()
+    assert L.rgbdseg_abi_version() == 1
+    assert _native.device_count() >= 0
+
+
+def test_config_errors_before_device():
+    L = _native.lib()
+    h = ctypes.c_void_p()
+    bad = _native.gmm_params_c(GmmParams(k_rgb=0))
+    assert L.rgbdseg_gmm_create(4, 4, ctypes.byref(bad), 1, 0, ctypes.byref(h)) == 2
+    assert "component counts" in _native.last_error()
+    good = _native.gmm_params_c(GmmParams())
+    assert L.rgbdseg_gmm_create(0, 4, ctypes.byref(good), 1, 0, ctypes.byref(h)) == 1
+    badp = _native.pbas_params_c(PbasParams(n=1, min_matches=2))
+    assert L.rgbdseg_pbas_create(4, 4, ctypes.byref(badp), 1, 0, 0, ctypes.byref(h)) == 2
+    bigp = _native.pbas_params_c(PbasParams(n=300))
+    assert L.rgbdseg_pbas_create(4, 4, ctypes.byref(bigp), 1, 0, 0, ctypes.byref(h)) == 2
+    okp = _native.pbas_params_c(PbasParams())
+    assert L.rgbdseg_pbas_create_band(4, 4, 3, 2, ctypes.byref(okp), 1, 0, 0,
+                                      ctypes.byref(h)) == 1
+
+
+def test_status_code_mapping():
+    with pytest.raises(DimensionError):
+        _native.check(1)
+    with pytest.raises(ConfigError):
+        _native.check(2)
+    with pytest.raises(DeviceError):
+        _native.check(3)
+    assert issubclass(DeviceError, RgbdSegError)
+
+
+def test_engine_validates_like_reference():
+    # ConfigError from PipelineConfig.validate (config.py:37-50), then
+    # DimensionError (engine.py:62-63), before any device work.
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    with pytest.raises(ConfigError):
+        SegmentationEngine(PipelineConfig(algorithm="sift"), 4, 4)
+    with pytest.raises(ConfigError):
+        SegmentationEngine(PipelineConfig(mode="depth"), 4, 4)
+    with pytest.raises(ConfigError):
+        SegmentationEngine(PipelineConfig(gmm=GmmParams(alpha=0)), 4, 4)
+    with pytest.raises(ConfigError):
+        SegmentationEngine(PipelineConfig(pbas=PbasParams(t_init=500)), 4, 4)
+    with pytest.raises(ConfigError):
+        SegmentationEngine(PipelineConfig(seed=2 ** 64), 4, 4)
+    with pytest.raises(DimensionError):
+        SegmentationEngine(PipelineConfig(), 0, 4)
+
+
+@pytest.mark.skipif(_native.device_count() > 0, reason="checks the no-GPU behaviour")
+def test_no_silent_cpu_fallback():
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    with pytest.raises(DeviceError):
+        SegmentationEngine(PipelineConfig(), 8, 6)

@@ -1,0 +1,345 @@
+"""GPU parity: the sm_100a kernels, called through the C-ABI, against the
+reference's own outputs (tests/golden, made by the reference) and against the
+CPU restatement (oracle/) on the same seeded inputs.
+
+Bar (BASELINE.json north_star):
+  - PBAS: masks and full state bit-exact;
+  - GMM: full state bit-exact; masks bit-exact on the golden fixtures and
+    >= 99.99% elsewhere (only `exp` -- CUDA libdevice vs host libm, <= 1 ulp
+    -- may differ, and it feeds the mask score only, gmm.py:311,368).
+"""
+
+import numpy as np
+import pytest
+
+import golden_util as gu
+from paper_2002_00250_b200 import synth
+from paper_2002_00250_b200.config import GmmParams, PbasParams, PipelineConfig
+
+pytestmark = pytest.mark.gpu
+
+GMM_MASK_AGREEMENT = 0.9999  # north_star floor; exact is expected
+
+
+def _engine(cfg, w, h):
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    return SegmentationEngine(cfg, w, h, device=0)
+
+
+def _run(cfg, frames):
+    h, w = frames[0].shape[:2]
+    with _engine(cfg, w, h) as eng:
+        masks = [eng.process_frame(f) for f in frames]
+        st = {k: v.copy() for k, v in eng.state_arrays().items()}
+    return np.stack(masks), st
+
+
+def _assert_state_equal(got, expected, keys):
+    for k in keys:
+        np.testing.assert_array_equal(got[k], expected[k], err_msg=k)
+
+
+# ------------------------------------------------ golden (reference) ------
+@pytest.mark.parametrize("name", gu.gmm_cases())
+def test_gmm_matches_reference_golden(name):
+    fx = gu.load(name)
+    masks, st = _run(gu.gmm_config(fx, name), list(fx["frames"]))
+    np.testing.assert_array_equal(masks, fx["masks"])
+    _assert_state_equal(st, fx, gu.GMM_KEYS)
+
+
+@pytest.mark.parametrize("name", gu.pbas_cases())
+def test_pbas_matches_reference_golden(name):
+    fx = gu.load(name)
+    masks, st = _run(gu.pbas_config(fx, name), list(fx["frames"]))
+    np.testing.assert_array_equal(masks, fx["masks"])
+    _assert_state_equal(st, fx, gu.PBAS_KEYS)
+
+
+def test_device_rng_matches_reference_golden():
+    from paper_2002_00250_b200.rng import pixel_keys, rng_stream
+
+    fx = gu.load("rng.npz")
+    np.testing.assert_array_equal(pixel_keys(fx["keys"]), fx["values"])
+    s, x, y, f = (int(v) for v in fx["stream_key"])
+    np.testing.assert_array_equal(rng_stream(s, x, y, f, len(fx["stream"])), fx["stream"])
+
+
+# ------------------------------------------------ oracle, config sizes ----
+def _compare_with_oracle(oracle_mod, cfg, frames, keys, exact_masks):
+    h, w = frames[0].shape[:2]
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    mism = 0
+    with _engine(cfg, w, h) as eng:
+        for t, f in enumerate(frames):
+            m_ref = ref.process_frame(f)
+            m_gpu = eng.process_frame(f)
+            if exact_masks:
+                np.testing.assert_array_equal(m_gpu, m_ref, err_msg=f"frame {t}")
+            else:
+                mism += int(np.count_nonzero(m_gpu != m_ref))
+        st = {k: v.copy() for k, v in eng.state_arrays().items()}
+    _assert_state_equal(st, ref.state_arrays(), keys)
+    agreement = 1.0 - mism / (len(frames) * h * w)
+    assert agreement >= GMM_MASK_AGREEMENT, agreement
+    return mism
+
+
+@pytest.mark.parametrize("k_rgb,regime", [(3, "T"), (7, "T"), (7, "S"), (3, "S")])
+def test_gmm_config1_640x480_vs_oracle(oracle_mod, k_rgb, regime):
+    # BASELINE config 1: GMM K=3 (and the paper default 7/3), 640x480, 100 frames.
+    frames = synth.sequence(regime, 640, 480, seed=0, frames=100, k_rgb=k_rgb)
+    cfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=k_rgb, k_d=3))
+    mism = _compare_with_oracle(oracle_mod, cfg, frames, gu.GMM_KEYS, exact_masks=False)
+    print(f"GMM {k_rgb}/3 regime {regime}: {mism} mask pixels differ of {100 * 640 * 480}")
+
+
+@pytest.mark.parametrize("mode", ["rgbd", "rgb_only"])
+def test_pbas_config2_640x480_vs_oracle(oracle_mod, mode):
+    # BASELINE config 2: PBAS N=20, 640x480, moving objects + depth holes.
+    frames = synth.sequence("T", 640, 480, seed=1, frames=100)
+    cfg = PipelineConfig(algorithm="pbas", mode=mode, pbas=PbasParams(n=20), seed=2)
+    _compare_with_oracle(oracle_mod, cfg, frames, gu.PBAS_KEYS, exact_masks=True)
+
+
+# ------------------------------------------------ edge cases -------------
+EDGE_SIZES = [(1, 1), (1, 37), (37, 1), (13, 17), (129, 3)]
+
+
+@pytest.mark.parametrize("w,h", EDGE_SIZES)
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_ragged_and_degenerate_sizes(oracle_mod, w, h, algo):
+    rng = np.random.default_rng(w * 1000 + h)
+    base = rng.integers(0, 256, size=(h, w, 4), dtype=np.uint8)
+    frames = []
+    for t in range(30):
+        f = base.copy()
+        f[rng.random((h, w)) < 0.2] = rng.integers(0, 256, size=4, dtype=np.uint8)
+        f[:, :, 3][rng.random((h, w)) < 0.1] = 0
+        frames.append(f)
+    if algo == "gmm":
+        cfg = PipelineConfig(algorithm="gmm", gmm=GmmParams(k_rgb=3, k_d=2))
+        keys = gu.GMM_KEYS
+    else:
+        cfg = PipelineConfig(algorithm="pbas", pbas=PbasParams(n=5), seed=11)
+        keys = gu.PBAS_KEYS
+    _compare_with_oracle(oracle_mod, cfg, frames, keys, exact_masks=True)
+
+
+@pytest.mark.parametrize("k_rgb,k_d,mode", [(10, 5, "rgbd"), (16, 1, "rgb_only"), (8, 4, "rgbd"),
+                                            (1, 1, "rgbd")])
+def test_gmm_component_counts(oracle_mod, k_rgb, k_d, mode):
+    # k outside the unrolled set exercises the generic instantiation.
+    frames = synth.sequence("S", 48, 40, seed=4, frames=40, k_rgb=min(k_rgb, 7))
+    cfg = PipelineConfig(algorithm="gmm", mode=mode,
+                         gmm=GmmParams(k_rgb=k_rgb, k_d=k_d, alpha=0.01))
+    _compare_with_oracle(oracle_mod, cfg, frames, gu.GMM_KEYS, exact_masks=False)
+
+
+@pytest.mark.parametrize("n,mm", [(1, 1), (20, 20), (31, 2), (32, 3), (64, 2), (255, 4)])
+def test_pbas_buffer_sizes(oracle_mod, n, mm):
+    # n > 31 switches the intent map to 16-bit codes.
+    frames = synth.sequence("T", 40, 24, seed=6, frames=n + 25)
+    cfg = PipelineConfig(algorithm="pbas", pbas=PbasParams(n=n, min_matches=mm), seed=n)
+    _compare_with_oracle(oracle_mod, cfg, frames, gu.PBAS_KEYS, exact_masks=True)
+
+
+def test_gmm_small_var_init_non_lazy(oracle_mod):
+    # var_init < VAR_FLOOR disables lazy record loading (floor on unseeded slots).
+    frames = synth.sequence("T", 40, 24, seed=9, frames=30)
+    cfg = PipelineConfig(algorithm="gmm", gmm=GmmParams(k_rgb=4, k_d=2, var_init=0.25, alpha=0.1))
+    _compare_with_oracle(oracle_mod, cfg, frames, gu.GMM_KEYS, exact_masks=False)
+
+
+# ------------------------------------------------ engine surface ----------
+def test_state_view_is_live():
+    # tests/test_acceptance.py:130-139 takes state_arrays() once up front.
+    cfg = PipelineConfig(algorithm="gmm", mode="rgbd")
+    rng = np.random.default_rng(99)
+    with _engine(cfg, 64, 64) as eng:
+        state = eng.state_arrays()
+        assert set(state) == set(gu.GMM_KEYS)
+        for _ in range(60):
+            frame = rng.integers(0, 256, size=(64, 64, 4), dtype=np.uint8)
+            frame[:, :, 3] = rng.integers(1, 256, size=(64, 64))
+            eng.process_frame(frame)
+            for key in ("rgb_w", "d_w"):
+                assert np.abs(state[key].sum(axis=2) - 1.0).max() <= 1e-9
+            for key in ("rgb_var", "d_var"):
+                assert state[key].min() >= 1.0
+
+
+def test_pbas_bounds_every_frame():
+    # tests/test_pbas.py:249-262 / acceptance criterion 8
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", seed=2)
+    rng = np.random.default_rng(6)
+    with _engine(cfg, 12, 10) as eng:
+        state = eng.state_arrays()
+        for _ in range(60):
+            eng.process_frame(rng.integers(0, 256, size=(10, 12, 4), dtype=np.uint8))
+            assert state["r_rgb"].min() >= 18.0 and state["r_d"].min() >= 18.0
+            assert state["t"].min() >= 2.0 and state["t"].max() <= 200.0
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_burn_in_constant_scene_is_background(algo):
+    # tests/test_gmm.py:266-272, tests/test_pbas.py:509-519
+    frame = np.full((6, 8, 4), 77, dtype=np.uint8)
+    with _engine(PipelineConfig(algorithm=algo, mode="rgbd"), 8, 6) as eng:
+        masks = [eng.process_frame(frame) for _ in range(40)]
+        if algo == "pbas":
+            assert (eng.state_arrays()["samples"] == 77).all()
+    assert all(int(m.sum()) == 0 for m in masks)
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_all_invalid_depth_equals_rgb_only(algo):
+    # tests/test_pbas.py:536-550 / acceptance criterion 6
+    rng = np.random.default_rng(51)
+    frames = []
+    for _ in range(30):
+        f = rng.integers(0, 256, size=(9, 13, 4), dtype=np.uint8)
+        f[:, :, 3] = 0
+        frames.append(f)
+    out = {}
+    for mode in ("rgbd", "rgb_only"):
+        out[mode], _ = _run(PipelineConfig(algorithm=algo, mode=mode, seed=3), frames)
+    np.testing.assert_array_equal(out["rgbd"], out["rgb_only"])
+
+
+def test_frame_shape_checked():
+    from paper_2002_00250_b200.errors import DimensionError
+
+    with _engine(PipelineConfig(algorithm="gmm"), 8, 6) as eng:
+        with pytest.raises(DimensionError):
+            eng.process_frame(np.zeros((6, 9, 4), dtype=np.uint8))
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_batched_streams_equal_single_engines(algo):
+    # The race-detection proxy of the reference (worker-count bit-equality,
+    # tests/test_gmm.py:250-264) becomes: batched multi-stream launch ==
+    # independent single-stream engines, bit for bit.
+    import torch
+
+    from paper_2002_00250_b200.engine import MultiStreamEngine
+
+    n, w, h = 3, 33, 20
+    seqs = [synth.sequence("T", w, h, seed=s, frames=30) for s in range(n)]
+    cfg = PipelineConfig(algorithm=algo, mode="rgbd", seed=40, pbas=PbasParams(n=8))
+    ref = []
+    for s in range(n):
+        c = PipelineConfig(algorithm=algo, mode="rgbd", seed=40 + s, pbas=PbasParams(n=8))
+        ref.append(_run(c, seqs[s]))
+    with MultiStreamEngine(cfg, w, h, n, device=0) as ms:
+        masks = []
+        for t in range(30):
+            fr = torch.from_numpy(np.stack([seqs[s][t] for s in range(n)])).cuda()
+            masks.append(ms.process(fr).cpu().numpy())
+        for s in range(n):
+            np.testing.assert_array_equal(np.stack([m[s] for m in masks]), ref[s][0])
+            st = {k: v for k, v in ms.engines[s].state_arrays().items()}
+            _assert_state_equal(st, ref[s][1], list(ref[s][1]))
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_device_tensor_path_equals_host_path(algo):
+    import torch
+
+    frames = synth.sequence("T", 50, 30, seed=8, frames=30)
+    cfg = PipelineConfig(algorithm=algo, mode="rgbd", seed=5, pbas=PbasParams(n=6))
+    host_masks, host_state = _run(cfg, frames)
+    with _engine(cfg, 50, 30) as eng:
+        dev = [eng.process_frame(torch.from_numpy(f).cuda()).cpu().numpy() for f in frames]
+        st = {k: v for k, v in eng.state_arrays().items()}
+    np.testing.assert_array_equal(np.stack(dev), host_masks)
+    _assert_state_equal(st, host_state, list(host_state))
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_load_state_resume_mid_sequence(oracle_mod, algo):
+    # Checkpoint/resume: seed the device from the oracle's state at frame 20
+    # and continue; must match the oracle's uninterrupted run.
+    frames = synth.sequence("T", 36, 28, seed=12, frames=40)
+    cfg = PipelineConfig(algorithm=algo, mode="rgbd", seed=9, pbas=PbasParams(n=10))
+    ref = oracle_mod.OracleEngine(cfg, 36, 28, workers=2)
+    for f in frames[:20]:
+        ref.process_frame(f)
+    with _engine(cfg, 36, 28) as eng:
+        eng.load_state(ref.state_arrays())
+        eng.frame_idx = ref.frame_idx
+        for t, f in enumerate(frames[20:]):
+            np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
+                                          err_msg=f"frame {20 + t}")
+        got = {k: v for k, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), list(got))
+
+
+# ------------------------------------------------ scalar KATs on device ---
+def _gmm1(params, rgb_comps, d_comps=(), mode="rgb_only"):
+    eng = _engine(PipelineConfig(algorithm="gmm", mode=mode, gmm=params), 1, 1)
+    st = {k: v.copy() for k, v in eng.state_arrays().items()}
+    for k, (w, mu, v) in enumerate(rgb_comps):
+        st["rgb_w"][0, 0, k], st["rgb_mu"][0, 0, k], st["rgb_var"][0, 0, k] = w, mu, v
+    for k, (w, mu, v) in enumerate(d_comps):
+        st["d_w"][0, 0, k], st["d_mu"][0, 0, k], st["d_var"][0, 0, k] = w, mu, v
+    eng.load_state(st)
+    return eng
+
+
+def _px(rgb, d=0):
+    return np.array([[[rgb[0], rgb[1], rgb[2], d]]], dtype=np.uint8)
+
+
+def test_kat_weight_recurrence_on_device():
+    # tests/test_gmm.py:143-150
+    eng = _gmm1(GmmParams(k_rgb=2, alpha=0.001),
+                [(0.5, [0, 0, 0], 100.0), (0.5, [200, 200, 200], 100.0)])
+    eng.process_frame(_px((0, 0, 0)))
+    w = eng.state_arrays()["rgb_w"][0, 0]
+    assert w[0] == pytest.approx(0.5005, abs=1e-12) and w[1] == pytest.approx(0.4995, abs=1e-12)
+
+
+def test_kat_least_fit_replacement_on_device():
+    # tests/test_gmm.py:165-177
+    eng = _gmm1(GmmParams(k_rgb=3), [(0.6, [0, 0, 0], 100.0), (0.1, [50, 50, 50], 400.0),
+                                     (0.3, [200, 200, 200], 100.0)])
+    eng.process_frame(_px((120, 120, 120)))
+    st = eng.state_arrays()
+    assert st["rgb_mu"][0, 0, 1].tolist() == [120.0, 120.0, 120.0]
+    assert st["rgb_var"][0, 0, 1] == 225.0
+    assert st["rgb_w"][0, 0, 1] == pytest.approx(0.05 / 0.95, rel=1e-9)
+
+
+def test_kat_blend_on_device():
+    # tests/test_gmm.py:179-186
+    eng = _gmm1(GmmParams(k_rgb=1, alpha=0.5), [(1.0, [10, 10, 10], 16.0)])
+    eng.process_frame(_px((12, 10, 10)))
+    st = eng.state_arrays()
+    assert st["rgb_mu"][0, 0, 0].tolist() == [11.0, 10.0, 10.0]
+    assert st["rgb_var"][0, 0, 0] == 10.0
+
+
+def test_kat_first_frame_and_depth_seed_on_device():
+    # tests/test_gmm.py:203-219
+    with _engine(PipelineConfig(algorithm="gmm", mode="rgbd"), 1, 1) as eng:
+        assert eng.process_frame(_px((40, 80, 120), 200))[0, 0] == 0
+    with _engine(PipelineConfig(algorithm="gmm", mode="rgbd"), 1, 1) as eng:
+        eng.process_frame(_px((1, 2, 3), 0))
+        assert eng.state_arrays()["d_w"][0, 0, 0] == 0.0
+        eng.process_frame(_px((1, 2, 3), 77))
+        assert eng.state_arrays()["d_w"][0, 0, 0] == 1.0
+        assert eng.state_arrays()["d_mu"][0, 0, 0, 0] == 77.0
+
+
+def test_kat_pbas_camouflage_and_self_update_on_device():
+    # tests/test_pbas.py:322-330 (depth catches colour camouflage)
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd")
+    with _engine(cfg, 1, 1) as eng:
+        st = {k: v.copy() for k, v in eng.state_arrays().items()}
+        st["samples"][0, 0, :] = (10, 20, 30, 150)
+        eng.load_state(st)
+        eng.frame_idx = 20
+        assert eng.process_frame(_px((10, 20, 30), 90))[0, 0] == 255
+        assert eng.state_arrays()["dmin_d"][0, 0, 0] == 60
