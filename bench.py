@@ -253,7 +253,8 @@ def run_ours(args, rank, world, local_rank):
         ring_t = torch.from_numpy(_gen_ring("T", w, h, stream_ids, 8)).to(dev)
         algos.append(("pbas", p, ring_t, B_ALG.get(("pbas", pbas_n))))
     masks = torch.empty((S, h, w), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # dedicated stream: every launch and event is ordered on it
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
     mbase = masks.data_ptr()
     mptrs = [mbase + i * npix for i in range(S)]

@@ -64,6 +64,20 @@ def _is_torch(x) -> bool:
     return type(x).__module__.split(".")[0] == "torch"
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the C-ABI reads a NULL stream as "the handle's own"
+
+
+def torch_stream_handle(device=None) -> int:
+    """cudaStream_t of torch's current stream, as the C-ABI expects it.
+
+    torch reports its default (legacy NULL) stream as 0, which the C-ABI
+    would read as "the handle's own stream"; pass cudaStreamLegacy instead
+    so the kernels stay ordered with torch's work."""
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream or CUDA_STREAM_LEGACY
+
+
 class _Handle:
     """Owns one C-ABI handle (GMM or PBAS)."""
 
@@ -242,7 +256,7 @@ class SegmentationEngine:
             raise DeviceError(f"frame is on {frame.device}, engine on cuda:{self.device}")
         frame = frame.contiguous()
         mask = torch.empty((self.rows, self.width), dtype=torch.uint8, device=frame.device)
-        stream = torch.cuda.current_stream(frame.device).cuda_stream
+        stream = torch_stream_handle(frame.device)
         self.step_device(frame.data_ptr(), mask.data_ptr(), stream)
         return mask
 
@@ -340,7 +354,7 @@ class MultiStreamEngine:
         fb, mb = frames.data_ptr(), masks.data_ptr()
         fs, ms = self.height * self.width * 4, self.height * self.width
         self.step_ptrs([fb + i * fs for i in range(self.n)], [mb + i * ms for i in range(self.n)],
-                       torch.cuda.current_stream(frames.device).cuda_stream)
+                       torch_stream_handle(frames.device))
         return masks
 
     def close(self):
