@@ -135,7 +135,7 @@ def _gen_ring(regime, w, h, seeds, ring, k_rgb=7):
 
 
 # --------------------------------------------------------- CPU baseline ----
-def cpu_sample(w, h, gmm_k, pbas_n, seed, budget_s=12.0, max_frames=12, workers=None):
+def cpu_sample(w, h, gmm_k, pbas_n, seed, budget_s=12.0, max_frames=400, workers=None):
     """Time the oracle port (reference algorithm, CPU) on a bounded sample:
     one w x h stream, GMM + PBAS per frame, after an untimed burn-in."""
     from oracle import oracle
