@@ -172,6 +172,17 @@ int rgbdseg_pbas_step(rgbdseg_pbas* h, const uint8_t* frame_dev, uint8_t* mask_d
 int rgbdseg_pbas_classify(rgbdseg_pbas* h, const uint8_t* frame_dev, uint8_t* mask_dev,
                           void* stream);
 int rgbdseg_pbas_apply(rgbdseg_pbas* h, const uint8_t* frame_dev, void* stream);
+/* Classify only band rows [row0, row1) (same frame, same frame_idx): lets a
+ * row band classify its two edge rows first and overlap the halo exchange
+ * with the interior.  Every row must be classified before apply. */
+int rgbdseg_pbas_classify_rows(rgbdseg_pbas* h, const uint8_t* frame_dev, uint8_t* mask_dev,
+                               int32_t row0, int32_t row1, void* stream);
+/* Copy the band's first/last intent-code rows out (device to device, W codes
+ * each; NULL skips), and set the halo rows from the neighbours' copies (NULL
+ * = no neighbour: "no intent").  Stream-ordered. */
+int rgbdseg_pbas_copy_edges(rgbdseg_pbas* h, void* first_dst, void* last_dst, void* stream);
+int rgbdseg_pbas_set_halos(rgbdseg_pbas* h, const void* above_src, const void* below_src,
+                           void* stream);
 /* Device pointers of the intent rows: the band's first/last own rows and
  * the halo rows above/below it; each row is row_bytes long.  Halo rows hold
  * "no intent" unless the caller fills them between classify and apply. */

@@ -52,6 +52,9 @@ def lib():
     L.oracle_pbas_band.restype = i64
     L.oracle_pbas_band.argtypes = ([i64, i64, vp, i64, i64, i64] + [vp] * 10 + [u64, i32, i32]
                                    + [f64] * 7 + [i32, vp, vp])
+    L.oracle_pbas_band_emit.restype = i64
+    L.oracle_pbas_band_emit.argtypes = ([i64, i64, vp, i64, i64, i64] + [vp] * 10 + [u64, i32, i32]
+                                        + [f64] * 7 + [i32, vp, vp, vp])
     L.oracle_pbas_frame.restype = i64
     L.oracle_pbas_frame.argtypes = ([i64, i64, vp, i64] + [vp] * 10 + [u64, i32, i32]
                                     + [f64] * 7 + [i32, vp, i32])
@@ -183,6 +186,26 @@ class OracleEngine:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def pbas_band_emit(cfg, state, frame, frame_idx, y0, y1, mask):
+    """One PBAS row band with global coordinates (pbas.py:344-508); returns
+    (intents (k,3) = (ny, nx, slot), emitters (k,2) = (y, x)) in emission order."""
+    h, w = frame.shape[:2]
+    p = cfg.pbas
+    cap = max((y1 - y0) * w, 1)
+    intents = np.empty((cap, 3), dtype=np.int64)
+    emitters = np.empty((cap, 2), dtype=np.int64)
+    st = state
+    k = lib().oracle_pbas_band_emit(
+        w, h, _p(frame), frame_idx, y0, y1,
+        _p(st["samples"]), _p(st["dmin_rgb"]), _p(st["dmin_d"]),
+        _p(st["len_rgb"]), _p(st["pos_rgb"]), _p(st["len_d"]), _p(st["pos_d"]),
+        _p(st["r_rgb"]), _p(st["r_d"]), _p(st["t"]),
+        int(cfg.seed) & _MASK64, p.n, p.min_matches,
+        p.r_lower, p.r_scale, p.r_inc_dec, p.t_lower, p.t_upper, p.t_inc, p.t_dec,
+        int(cfg.mode == "rgbd"), _p(mask), _p(intents), _p(emitters))
+    return intents[:k], emitters[:k]
 
 
 def cpu_threads() -> int:

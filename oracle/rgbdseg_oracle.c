@@ -184,7 +184,8 @@ static inline int64_t iabs64(int64_t v) { return v < 0 ? -v : v; }
 
 /* pbas.py:344-508 (_pbas_band) over rows [y0, y1) with GLOBAL coordinates;
  * intents (ny, nx, slot) are appended in row-major emission order. */
-static int64_t pbas_band(const pbas_args* a, int64_t y0, int64_t y1, int64_t* intents) {
+static int64_t pbas_band(const pbas_args* a, int64_t y0, int64_t y1, int64_t* intents,
+                         int64_t* emitters) {
     const int64_t width = a->width, height = a->height, n = a->n;
     int64_t n_intents = 0;
     for (int64_t y = y0; y < y1; ++y) {
@@ -316,6 +317,10 @@ static int64_t pbas_band(const pbas_args* a, int64_t y0, int64_t y1, int64_t* in
                                 intents[n_intents * 3 + 0] = ny;
                                 intents[n_intents * 3 + 1] = nx;
                                 intents[n_intents * 3 + 2] = slot;
+                                if (emitters) { /* test hook: who asked (row-band halo tests) */
+                                    emitters[n_intents * 2 + 0] = y;
+                                    emitters[n_intents * 2 + 1] = x;
+                                }
                                 n_intents += 1;
                                 break;
                             }
@@ -357,7 +362,25 @@ int64_t oracle_pbas_band(int64_t width, int64_t height, const uint8_t* frame, in
                    len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
                    seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
                    t_upper, t_inc, t_dec,   use_depth, mask};
-    return pbas_band(&a, y0, y1, intents);
+    return pbas_band(&a, y0, y1, intents, NULL);
+}
+
+/* Same as oracle_pbas_band, also recording each intent's emitter (y, x):
+ * used by the row-band halo tests to rebuild per-emitter intent codes. */
+int64_t oracle_pbas_band_emit(int64_t width, int64_t height, const uint8_t* frame,
+                              int64_t frame_idx, int64_t y0, int64_t y1, uint8_t* samples,
+                              uint8_t* dmin_rgb, uint8_t* dmin_d, uint8_t* len_rgb,
+                              uint8_t* pos_rgb, uint8_t* len_d, uint8_t* pos_d, double* r_rgb,
+                              double* r_d, double* t, uint64_t seed, int32_t n,
+                              int32_t min_matches, double r_lower, double r_scale,
+                              double r_inc_dec, double t_lower, double t_upper, double t_inc,
+                              double t_dec, int32_t use_depth, uint8_t* mask, int64_t* intents,
+                              int64_t* emitters) {
+    pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
+                   len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
+                   seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
+                   t_upper, t_inc, t_dec,   use_depth, mask};
+    return pbas_band(&a, y0, y1, intents, emitters);
 }
 
 /* ------------------------------------------------- multi-threaded frames - */
@@ -396,7 +419,7 @@ static void* band_worker(void* p) {
                         j->rgb_var, j->d_w, j->d_mu, j->d_var, j->k_rgb, j->k_d, j->alpha, j->s,
                         j->tau, j->lam2, j->var_init, j->w_init, j->use_depth, j->mask);
     else
-        j->count = pbas_band(j->pa, j->y0, j->y1, j->intents);
+        j->count = pbas_band(j->pa, j->y0, j->y1, j->intents, NULL);
     return NULL;
 }
 

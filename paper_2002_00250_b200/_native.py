@@ -26,6 +26,7 @@ EXPORTS = (
     "rgbdseg_gmm_read_state", "rgbdseg_gmm_write_state", "rgbdseg_gmm_stream",
     "rgbdseg_pbas_create", "rgbdseg_pbas_create_band", "rgbdseg_pbas_destroy",
     "rgbdseg_pbas_step", "rgbdseg_pbas_classify", "rgbdseg_pbas_apply", "rgbdseg_pbas_halo_ptrs",
+    "rgbdseg_pbas_classify_rows", "rgbdseg_pbas_copy_edges", "rgbdseg_pbas_set_halos",
     "rgbdseg_pbas_step_batch", "rgbdseg_pbas_process_host", "rgbdseg_pbas_sync",
     "rgbdseg_pbas_get_frame_idx", "rgbdseg_pbas_set_frame_idx", "rgbdseg_pbas_state_bytes",
     "rgbdseg_pbas_read_state", "rgbdseg_pbas_write_state", "rgbdseg_pbas_stream",
@@ -84,6 +85,9 @@ def _declare(L):
         "rgbdseg_pbas_classify": (ctypes.c_int, [vp, vp, vp, vp]),
         "rgbdseg_pbas_apply": (ctypes.c_int, [vp, vp, vp]),
         "rgbdseg_pbas_halo_ptrs": (ctypes.c_int, [vp, P(vp), P(vp), P(vp), P(vp), P(i64)]),
+        "rgbdseg_pbas_classify_rows": (ctypes.c_int, [vp, vp, vp, i32, i32, vp]),
+        "rgbdseg_pbas_copy_edges": (ctypes.c_int, [vp, vp, vp, vp]),
+        "rgbdseg_pbas_set_halos": (ctypes.c_int, [vp, vp, vp, vp]),
         "rgbdseg_pbas_step_batch": (ctypes.c_int, [vp, i32, vp, vp, vp]),
         "rgbdseg_pbas_process_host": (ctypes.c_int, [vp, vp, vp, i32]),
         "rgbdseg_pbas_sync": (ctypes.c_int, [vp]),

@@ -53,6 +53,26 @@ struct DeviceGuard {
 // 256-byte boundary (full-sector, 256-bit-load friendly).
 inline int64_t plane_pitch(int64_t npix) { return (npix + 31) / 32 * 32; }
 
+// Granlund-Montgomery unsigned division by a runtime-constant d < 2^31
+// (host computes m, l once; exhaustively checked in tests/test_capi.py's
+// Python twin).  d == 1 is encoded as l == 0.
+struct UDivMagic {
+    uint32_t m;
+    int32_t l;
+};
+inline UDivMagic udiv_magic(uint32_t d) {
+    if (d <= 1) return {0u, 0};
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    const uint64_t m = ((1ull << 32) * ((1ull << l) - d)) / d + 1;
+    return {(uint32_t)m, l};
+}
+__device__ __forceinline__ uint32_t udiv(uint32_t n, UDivMagic g) {
+    if (g.l == 0) return n;
+    const uint32_t t = __umulhi(n, g.m);
+    return (t + ((n - t) >> 1)) >> (g.l - 1);
+}
+
 // ------------------------------------------------- counter-based RNG -----
 // Device twin of engine_rng.py:15-44 (SplitMix64 finalizer chain).  The
 // (seed, x, y, frame) prefix is shared by the three draws of a pixel
@@ -77,6 +97,15 @@ __host__ __device__ __forceinline__ uint64_t rng_prefix(uint64_t seed, uint64_t 
     h = mix64(h ^ (x * RNG_KX));
     h = mix64(h ^ (y * RNG_KY));
     return mix64(h ^ (f * RNG_KF));
+}
+
+// The first absorption depends on (seed, x) only: a per-column table of it
+// (computed once per handle) saves one mix per pixel; identical values.
+__host__ __device__ __forceinline__ uint64_t rng_column(uint64_t seed, uint64_t x) {
+    return mix64((seed ^ RNG_SALT) ^ (x * RNG_KX));
+}
+__host__ __device__ __forceinline__ uint64_t rng_prefix_col(uint64_t hcol, uint64_t y, uint64_t f) {
+    return mix64(mix64(hcol ^ (y * RNG_KY)) ^ (f * RNG_KF));
 }
 
 __host__ __device__ __forceinline__ double rng_draw(uint64_t prefix, uint64_t d) {

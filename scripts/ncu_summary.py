@@ -54,7 +54,7 @@ def main():
                 return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
 
             def to_s(v, u):
-                return float(v) * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}[u]
+                return float(v) * {"ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}[u]
 
             rb = to_bytes(*d["dram__bytes_read.sum"])
             wb = to_bytes(*d["dram__bytes_write.sum"])

@@ -93,3 +93,33 @@ def test_no_silent_cpu_fallback():
 
     with pytest.raises(DeviceError):
         SegmentationEngine(PipelineConfig(), 8, 6)
+
+
+def _udiv_magic(d):
+    """Python twin of csrc/common.cuh udiv_magic/udiv (Granlund-Montgomery)."""
+    if d <= 1:
+        return 0, 0
+    l = (d - 1).bit_length()
+    return ((1 << 32) * ((1 << l) - d)) // d + 1, l
+
+
+def _udiv(n, d):
+    m, l = _udiv_magic(d)
+    if l == 0:
+        return n
+    t = (n * m) >> 32
+    return (t + ((n - t) >> 1)) >> (l - 1)
+
+
+def test_magic_division_used_for_pixel_rows():
+    # K2 maps pixel index -> (row, column) with this 32-bit magic division.
+    import numpy as np
+
+    rng = np.random.default_rng(0)
+    widths = list(range(1, 3000)) + [7680, 3840, 1920, 1280, 640, 2 ** 31 - 1]
+    for d in widths:
+        m, _ = _udiv_magic(d)
+        assert m < 2 ** 32
+        ns = [0, 1, d - 1, d, d + 1, 2 ** 31 - 1] + [int(v) for v in rng.integers(0, 2 ** 31, 20)]
+        for n in ns:
+            assert _udiv(n, d) == n // d, (n, d)
