@@ -343,3 +343,24 @@ def test_kat_pbas_camouflage_and_self_update_on_device():
         eng.frame_idx = 20
         assert eng.process_frame(_px((10, 20, 30), 90))[0, 0] == 255
         assert eng.state_arrays()["dmin_d"][0, 0, 0] == 60
+
+
+@pytest.mark.parametrize("w,h,n", [(64, 24, 20), (96, 17, 5), (32, 40, 32), (64, 20, 33)])
+def test_pbas_deferred_intents_state_every_frame(oracle_mod, w, h, n):
+    # width % 32 == 0 and n <= 32 selects the deferred-intent mode (intents of
+    # frame t applied inside frame t+1's K2, flushed before state access);
+    # n = 33 takes the K3 path.  Reading the state after EVERY frame checks
+    # the flush against the reference semantics (intents applied at the end
+    # of each frame, engine.py:140-143).
+    frames = synth.sequence("T", w, h, seed=n, frames=n + 30)
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=n), seed=7 + n)
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    with _engine(cfg, w, h) as eng:
+        for t, f in enumerate(frames):
+            np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
+                                          err_msg=f"frame {t}")
+            if t >= n - 1 and t % 3 == 0:
+                np.testing.assert_array_equal(eng.state_arrays()["samples"],
+                                              ref.state_arrays()["samples"], err_msg=f"frame {t}")
+        got = {k: v for k, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
