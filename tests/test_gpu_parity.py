@@ -364,3 +364,49 @@ def test_pbas_deferred_intents_state_every_frame(oracle_mod, w, h, n):
                                               ref.state_arrays()["samples"], err_msg=f"frame {t}")
         got = {k: v for k, v in eng.state_arrays().items()}
     _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
+
+
+@pytest.mark.parametrize("nbands", [2, 3])
+def test_row_bands_on_one_gpu_match_oracle(oracle_mod, nbands):
+    # The config-5 split (bands.py) run on ONE device: each band is its own
+    # handle with global coordinates; the one-row intent halos move by
+    # device copies instead of NCCL.  Stitched masks and state must equal
+    # the single-frame reference run bit for bit.
+    import ctypes
+
+    import torch
+
+    from paper_2002_00250_b200 import _native
+    from paper_2002_00250_b200.bands import band_bounds
+    from paper_2002_00250_b200.engine import SegmentationEngine, torch_stream_handle
+
+    w, h, n = 45, 31, 6
+    frames = synth.sequence("T", w, h, seed=21, frames=n + 25)
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=n), seed=33)
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    bounds = band_bounds(h, nbands)
+    engines = [SegmentationEngine(cfg, w, h, device=0, _band=b) for b in bounds]
+    L = _native.lib()
+    rb = ctypes.c_int64()
+    L.rgbdseg_pbas_halo_ptrs(engines[0]._h.ptr, None, None, None, None, ctypes.byref(rb))
+    edges = torch.empty((nbands, 2, rb.value), dtype=torch.uint8, device="cuda")
+    st = ctypes.c_void_p(torch_stream_handle())
+    for t, f in enumerate(frames):
+        fr = torch.from_numpy(f).cuda()
+        mask = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+        for i, (e, (y0, y1)) in enumerate(zip(engines, bounds)):
+            fp = ctypes.c_void_p(fr[y0:y1].data_ptr())
+            mp = ctypes.c_void_p(mask[y0:y1].data_ptr())
+            _native.check(L.rgbdseg_pbas_classify_rows(e._h.ptr, fp, mp, 0, y1 - y0, st))
+            _native.check(L.rgbdseg_pbas_copy_edges(e._h.ptr, ctypes.c_void_p(edges[i, 0].data_ptr()),
+                                                    ctypes.c_void_p(edges[i, 1].data_ptr()), st))
+        for i, (e, (y0, y1)) in enumerate(zip(engines, bounds)):
+            above = ctypes.c_void_p(edges[i - 1, 1].data_ptr()) if i > 0 else None
+            below = ctypes.c_void_p(edges[i + 1, 0].data_ptr()) if i < nbands - 1 else None
+            _native.check(L.rgbdseg_pbas_set_halos(e._h.ptr, above, below, st))
+            _native.check(L.rgbdseg_pbas_apply(e._h.ptr, ctypes.c_void_p(fr[y0:y1].data_ptr()), st))
+        np.testing.assert_array_equal(mask.cpu().numpy(), ref.process_frame(f), err_msg=f"frame {t}")
+    for e, (y0, y1) in zip(engines, bounds):
+        for k, v in e.state_arrays().items():
+            np.testing.assert_array_equal(v, ref.state_arrays()[k][y0:y1], err_msg=f"{k} {y0}:{y1}")
+        e.close()
