@@ -64,6 +64,8 @@ WORKLOADS = {
     "config3": (1280, 720, 1, (7, 3), 20),
     "config1": (640, 480, 1, (3, 3), None),
     "config2": (640, 480, 1, None, 20),
+    # one 7680x4320 frame split into row bands, one per GPU (PBAS n=20)
+    "config5": (7680, 4320, 1, None, 20),
 }
 
 
@@ -386,6 +388,77 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
+def run_config5(args, rank, world, local_rank):
+    """BASELINE config 5: PBAS on one 7680x4320 stream, row bands across the
+    ranks (engine.py:48-50 split), one-row intent halo over NCCL per frame
+    (bands.RowBandPbas).  value = Mpixel/s of the whole frame."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2002_00250_b200.bands import RowBandPbas
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w, h, _, _, n = WORKLOADS["config5"]
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=n), seed=1)
+    band = RowBandPbas(cfg, w, h, rank, world, device=local_rank)
+    y0, y1 = band.y0, band.y1
+    ring = torch.from_numpy(_gen_ring("T", w, h, [0], 4)[0][:, y0:y1].copy()).to(dev)
+    mask = torch.empty((y1 - y0, w), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    t = 0
+    for _ in range(2 * n):  # burn-in: warm-up fill + full dmin rings
+        band.step(ring[t % 4], mask)
+        t += 1
+    for _ in range(args.warmup):
+        band.step(ring[t % 4], mask)
+        t += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(int(os.environ.get("RGBDSEG_NVSMI_INDEX", local_rank)))
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(args.steps):
+        band.step(ring[t % 4], mask)
+        t += 1
+    end.record(stream)
+    torch.cuda.synchronize()
+    clock_info = clocks.stop()
+    ms = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(ms.item())
+    peak, peak_kind = measured_peaks()
+    band_px = (y1 - y0) * w
+    achieved = B_ALG[("pbas", n)] * band_px * args.steps / (elapsed_ms / 1e3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": w * h * args.steps / (elapsed_ms / 1e3) / 1e6, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8/f64", "data": "synthetic (SURVEY.md §8(d) regime T)",
+            "config": {"workload": f"config5: PBAS n={n} on one {w}x{h} RGB-D stream, "
+                                   f"{world} row band(s), 1-row intent halo over NCCL",
+                       "width": w, "height": h, "bands": world,
+                       "l2": "inputs larger than L2 (PBAS state 4.9 GB)",
+                       "parallelism": f"row bands x{world} (engine.py:48-50 split)"},
+            "fps": args.steps / (elapsed_ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "pbas_classify (K2) + pbas_apply (K3), rank 0 band"},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": args.steps * (2 if world == 1 else 4),
+            "clocks": clock_info,
+        }
+        print(json.dumps(line), flush=True)
+    band.close()
+    return 0
+
+
 def run_e2e(args, algos, S, w, h, dev, world):
     """Same workload through SegmentationEngine.submit (host buffers): per
     step every stream's frame is copied H2D from pinned memory for each
@@ -462,6 +535,8 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
+        if args.workload == "config5":
+            return run_config5(args, rank, world, local_rank)
         return run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
