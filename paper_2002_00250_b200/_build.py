@@ -54,15 +54,20 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Compile csrc/*.cu into `out` (default: the in-tree librgbdseg_b200.so).
+    `defines` (e.g. ["PBAS_MIN_BLOCKS=6"]) builds tuning variants."""
+    if out is None and not defines and not force and not _stale():
         return LIB
+    lib_out = Path(out) if out is not None else LIB
+    build_dir = BUILD if not defines else BUILD / ("v_" + "_".join(d.replace("=", "") for d in defines))
     nvcc = _nvcc()
-    BUILD.mkdir(parents=True, exist_ok=True)
+    build_dir.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_one(src: Path):
-        obj = BUILD / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = build_dir / (src.stem + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *dflags, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
@@ -71,17 +76,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     jobs = min(len(sources()), os.cpu_count() or 4)
     with ThreadPoolExecutor(max_workers=jobs) as ex:
         results = list(ex.map(compile_one, sources()))
-    (BUILD / "ptxas.log").write_text("".join(log for _, log in results))
-    tmp = LIB.with_suffix(".so.tmp")
+    (build_dir / "ptxas.log").write_text("".join(log for _, log in results))
+    tmp = lib_out.with_suffix(".so.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp)]
     cmd += [str(o) for o, _ in results]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_out)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {lib_out}", file=sys.stderr)
+    return lib_out
 
 
 if __name__ == "__main__":

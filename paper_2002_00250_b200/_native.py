@@ -15,7 +15,8 @@ from pathlib import Path
 
 from .errors import ConfigError, DeviceError, DimensionError
 
-LIB_PATH = Path(__file__).resolve().parent / "librgbdseg_b200.so"
+LIB_PATH = Path(os.environ.get("RGBDSEG_B200_LIB") or
+                Path(__file__).resolve().parent / "librgbdseg_b200.so")
 
 # Every symbol include/rgbdseg_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
