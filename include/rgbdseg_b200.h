@@ -201,6 +201,15 @@ int rgbdseg_pbas_read_state(rgbdseg_pbas* h, int32_t field, void* host_dst, int6
 int rgbdseg_pbas_write_state(rgbdseg_pbas* h, int32_t field, const void* host_src, int64_t bytes);
 void* rgbdseg_pbas_stream(rgbdseg_pbas* h);
 
+/* ------------------------------------------------- input staging ------ */
+/* frames.scale_depth_map + resample_depth + pack_frame (src/rgbdseg/frames.py:46-88)
+ * on the device: rgb (H,W,3) u8 and depth16 (depth_h, depth_w) u16 (nearest-
+ * neighbour resampled to (H,W) when the sizes differ; NULL = rgb_only, depth
+ * byte 0, engine.py:199-200) -> packed frame (H,W,4) u8.  Bit-exact. */
+int rgbdseg_pack_frame(const uint8_t* rgb_dev, int32_t width, int32_t height,
+                       const uint16_t* depth16_dev, int32_t depth_w, int32_t depth_h,
+                       uint8_t* frame_dev, void* stream);
+
 /* ---------------------------------------------------- evaluation ------- */
 /* Confusion counts of a device mask against a device ground-truth label
  * plane (0 bg / 1 fg / 2 ignore; frames.py:27-29), accumulated into

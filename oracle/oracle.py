@@ -210,3 +210,39 @@ def pbas_band_emit(cfg, state, frame, frame_idx, y0, y1, mask):
 
 def cpu_threads() -> int:
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def scale_depth_map(depth16: np.ndarray) -> np.ndarray:
+    """frames.scale_depth_map (frames.py:46-52), numpy restatement."""
+    d = depth16.astype(np.uint32)
+    d8 = np.maximum((d * 255) // 65535, 1)
+    d8[depth16 == 0] = 0
+    return d8.astype(np.uint8)
+
+
+def resample_depth(depth16: np.ndarray, target_w: int, target_h: int) -> np.ndarray:
+    """frames.resample_depth (frames.py:73-88): nearest neighbour on pixel centres, f64 index."""
+    src_h, src_w = depth16.shape
+    if (src_w, src_h) == (target_w, target_h):
+        return depth16.copy()
+    ys = np.minimum(((np.arange(target_h) + 0.5) * src_h / target_h).astype(np.int64), src_h - 1)
+    xs = np.minimum(((np.arange(target_w) + 0.5) * src_w / target_w).astype(np.int64), src_w - 1)
+    return depth16[np.ix_(ys, xs)]
+
+
+def pack_frame(rgb: np.ndarray, depth16: np.ndarray | None) -> np.ndarray:
+    """frames.pack_frame (frames.py:55-70) after resampling depth to the RGB size."""
+    h, w = rgb.shape[:2]
+    frame = np.zeros((h, w, 4), dtype=np.uint8)
+    frame[:, :, :3] = rgb
+    if depth16 is not None:
+        frame[:, :, 3] = scale_depth_map(resample_depth(depth16, w, h))
+    return frame
+
+
+def compare_masks(result: np.ndarray, labels: np.ndarray):
+    """metrics.compare_masks (metrics.py:50-69): (tp, tn, fp, fn); label 2 = ignore."""
+    fg = result > 127
+    gt_fg, gt_bg = labels == 1, labels == 0
+    return (int(np.count_nonzero(fg & gt_fg)), int(np.count_nonzero(~fg & gt_bg)),
+            int(np.count_nonzero(fg & gt_bg)), int(np.count_nonzero(~fg & gt_fg)))

@@ -230,6 +230,16 @@ class SegmentationEngine:
         self._gmm_frame_idx += 1
         return mask
 
+    def apply(self, rgb, depth16=None):
+        """apply(rgb, depth) -> mask (the north_star's segmenter call): packs
+        RGB + 16-bit depth on the device (frames.py:46-88; depth resampled
+        to the RGB size when needed, None = no depth) and segments the frame.
+        Returns a CUDA (H, W) uint8 mask tensor."""
+        from .frames import pack_frame
+
+        frame = pack_frame(rgb, depth16, device=self.device)
+        return self.process_frame(frame)
+
     def submit(self, frame: np.ndarray, mask_out: np.ndarray) -> None:
         """Asynchronous host path: enqueue H2D + step + D2H into `mask_out`
         and return.  Both buffers must stay alive (and should be pinned) until

@@ -21,6 +21,9 @@ Fixtures:
                           synthetic regime T / S sequences through the
                           reference numba SegmentationEngine (engine.py:60-112),
                           all masks + final state_arrays().
+  frames.npz              frames.pack_frame(rgb, resample_depth(d16, W, H))
+                          (frames.py:46-88): all 65536 depth values plus
+                          up/down/odd mixed-resolution pairs
 """
 
 from __future__ import annotations
@@ -169,9 +172,30 @@ def make_pbas_seq():
                                params.t_dec]), **st)
 
 
+def make_frames():
+    """frames.pack_frame / scale_depth_map / resample_depth (frames.py:46-88)."""
+    from rgbdseg import frames as ref_frames
+
+    rng = np.random.default_rng(11)
+    out = {}
+    # every 16-bit depth value once (tests/test_frames.py:27-52 is exhaustive too)
+    d_all = np.arange(65536, dtype=np.uint16).reshape(256, 256)
+    rgb = rng.integers(0, 256, size=(256, 256, 3), dtype=np.uint8)
+    out["all_rgb"], out["all_d16"] = rgb, d_all
+    out["all_frame"] = ref_frames.pack_frame(rgb, d_all)
+    for tag, (w, h), (dw, dh) in (("up", (64, 48), (32, 24)), ("odd", (37, 23), (16, 11)),
+                                   ("down", (40, 30), (64, 48)), ("p720_480", (128, 72), (64, 48))):
+        rgb = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+        d16 = rng.integers(0, 65536, size=(dh, dw), dtype=np.uint16)
+        d16[rng.random((dh, dw)) < 0.1] = 0
+        out[f"{tag}_rgb"], out[f"{tag}_d16"] = rgb, d16
+        out[f"{tag}_frame"] = ref_frames.pack_frame(rgb, ref_frames.resample_depth(d16, w, h))
+    _save("frames.npz", **out)
+
+
+MAKERS = {"rng": make_rng, "gmm_equiv": make_gmm_equiv, "pbas_equiv": make_pbas_equiv,
+          "gmm_seq": make_gmm_seq, "pbas_seq": make_pbas_seq, "frames": make_frames}
+
 if __name__ == "__main__":
-    make_rng()
-    make_gmm_equiv()
-    make_pbas_equiv()
-    make_gmm_seq()
-    make_pbas_seq()
+    for name in (sys.argv[1:] or MAKERS):
+        MAKERS[name]()

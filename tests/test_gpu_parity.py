@@ -410,3 +410,39 @@ def test_row_bands_on_one_gpu_match_oracle(oracle_mod, nbands):
         for k, v in e.state_arrays().items():
             np.testing.assert_array_equal(v, ref.state_arrays()[k][y0:y1], err_msg=f"{k} {y0}:{y1}")
         e.close()
+
+
+# ------------------------------------------------ next rows: staging + eval
+@pytest.mark.parametrize("tag", ["all", "up", "odd", "down", "p720_480"])
+def test_device_pack_frame_matches_reference(tag):
+    # frames.py:46-88 on the device, against frames the reference packed
+    from paper_2002_00250_b200.frames import pack_frame
+
+    fx = gu.load("frames.npz")
+    got = pack_frame(fx[f"{tag}_rgb"], fx[f"{tag}_d16"]).cpu().numpy()
+    np.testing.assert_array_equal(got, fx[f"{tag}_frame"])
+
+
+def test_apply_rgb_depth_equals_process_frame_on_packed(oracle_mod):
+    # apply(rgb, depth16) == process_frame(pack_frame(rgb, resample(depth16)))
+    rng = np.random.default_rng(3)
+    cfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=3, k_d=3))
+    w, h = 64, 40
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    with _engine(cfg, w, h) as eng:
+        for t in range(12):
+            rgb = rng.integers(0, 256, size=(h, w, 3), dtype=np.uint8)
+            d16 = rng.integers(0, 65536, size=(h // 2, w // 2), dtype=np.uint16)
+            d16[rng.random(d16.shape) < 0.1] = 0
+            got = eng.apply(rgb, d16).cpu().numpy()
+            np.testing.assert_array_equal(got, ref.process_frame(oracle_mod.pack_frame(rgb, d16)))
+
+
+def test_device_confusion_counts_match_compare_masks(oracle_mod):
+    from paper_2002_00250_b200.frames import confusion_counts
+
+    rng = np.random.default_rng(2024)
+    for shape in ((32, 32), (1080, 1920), (7, 5)):
+        mask = np.where(rng.random(shape) < 0.35, 255, 0).astype(np.uint8)
+        labels = rng.choice([0, 1, 2], size=shape, p=[0.5, 0.3, 0.2]).astype(np.uint8)
+        assert confusion_counts(mask, labels) == oracle_mod.compare_masks(mask, labels)

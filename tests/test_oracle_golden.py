@@ -168,3 +168,11 @@ def test_kat_pbas_R_and_T_adaptation(oracle_mod):
     st = eng.state_arrays()
     assert st["r_rgb"][0, 0] == pytest.approx(18.9, abs=1e-12)
     assert st["t"][0, 0] == pytest.approx(18.0 - 0.05 / 10.0, abs=1e-12)
+
+
+def test_oracle_pack_frame_matches_reference(oracle_mod):
+    # frames.pack_frame(rgb, resample_depth(d16, W, H)) produced by the reference
+    fx = gu.load("frames.npz")
+    for tag in ("all", "up", "odd", "down", "p720_480"):
+        np.testing.assert_array_equal(oracle_mod.pack_frame(fx[f"{tag}_rgb"], fx[f"{tag}_d16"]),
+                                      fx[f"{tag}_frame"], err_msg=tag)
