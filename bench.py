@@ -485,49 +485,54 @@ def run_config5(args, rank, world, local_rank):
 
 
 def run_e2e(args, algos, S, w, h, dev, world):
-    """Same workload through SegmentationEngine.submit (host buffers): per
-    step every stream's frame is copied H2D from pinned memory for each
-    algorithm and the mask read back D2H, all inside the timed region."""
+    """Same workload through the public host-buffer API: MultiCameraPipeline
+    (pipeline.py) over the already burned-in engines.  Every step copies each
+    camera's frame(s) H2D from pinned memory and every mask D2H, inside the
+    timed region; steps are double-buffered so copies overlap compute.  The
+    algorithms keep their own inputs (regime S for GMM, T for PBAS), so each
+    frame is uploaded once per algorithm, as in the device-resident run."""
     import torch
     import torch.distributed as dist
 
+    from paper_2002_00250_b200.pipeline import MultiCameraPipeline
+
     npix = w * h
     steps = max(3, min(args.steps, args.e2e_steps))
-    host = {}
+    pipe = MultiCameraPipeline({}, w, h, S, device=dev.index, engines={a[0]: a[1] for a in algos})
+    host_in = {}
     for name, eng, ring, _ in algos:
-        R = ring.shape[1]
-        pinned = torch.empty(ring.shape, dtype=torch.uint8, pin_memory=True)
-        pinned.copy_(ring)
-        outs = torch.empty((S, h, w), dtype=torch.uint8, pin_memory=True)
-        host[name] = (pinned, pinned.numpy(), outs, outs.numpy(), R)
+        pinned = torch.empty((ring.shape[1],) + tuple(ring.shape[:1]) + tuple(ring.shape[2:]),
+                             dtype=torch.uint8, pin_memory=True)
+        pinned.copy_(ring.transpose(0, 1))  # (R, S, H, W, 4): one batch per step
+        host_in[name] = pinned
+    host_out = [{a[0]: torch.empty((S, h, w), dtype=torch.uint8, pin_memory=True) for a in algos}
+                for _ in range(pipe.depth)]
 
     def step(t):
-        for name, eng, ring, _ in algos:
-            _, fr, _, mk, R = host[name]
-            for i in range(S):
-                eng.engines[i].submit(fr[i, t % R], mk[i])
-        for name, eng, _, _ in algos:
-            for e in eng.engines:
-                e.synchronize()
+        return pipe.submit({a[0]: host_in[a[0]][t % host_in[a[0]].shape[0]] for a in algos},
+                           host_out[t % pipe.depth])
 
-    for t in range(2):
+    for t in range(3):
         step(t)
-    torch.cuda.synchronize()
+    pipe.synchronize()
     if world > 1:
         dist.barrier()
+    h2d = 0
     t0 = time.perf_counter()
     for t in range(steps):
-        step(2 + t)
+        h2d = step(3 + t)
+    pipe.synchronize()
     dt = time.perf_counter() - t0
     tt = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt.item())
-    n_alg = len(algos)
     return {"value": npix * S * world * steps / dt / 1e6, "unit": UNIT,
-            "h2d_bytes_per_step": 4 * npix * S * n_alg, "d2h_bytes_per_step": npix * S * n_alg,
-            "steps": steps, "timing": "host perf_counter over synchronised steps (spans H2D+D2H)",
-            "api": "SegmentationEngine.submit/synchronize (pinned host buffers, one CUDA stream per engine)"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": npix * S * len(algos),
+            "steps": steps,
+            "timing": "host perf_counter from first submit to final synchronize (spans H2D+D2H)",
+            "api": "pipeline.MultiCameraPipeline.submit (pinned host buffers, double-buffered, "
+                   "copy-in / per-algorithm compute / copy-out streams)"}
 
 
 def main():

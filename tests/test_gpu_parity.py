@@ -446,3 +446,40 @@ def test_device_confusion_counts_match_compare_masks(oracle_mod):
         mask = np.where(rng.random(shape) < 0.35, 255, 0).astype(np.uint8)
         labels = rng.choice([0, 1, 2], size=shape, p=[0.5, 0.3, 0.2]).astype(np.uint8)
         assert confusion_counts(mask, labels) == oracle_mod.compare_masks(mask, labels)
+
+
+@pytest.mark.parametrize("shared", [True, False])
+def test_multicamera_pipeline_matches_single_engines(shared):
+    # pipeline.MultiCameraPipeline (double-buffered H2D / compute / D2H) must
+    # produce, frame by frame, exactly what independent engines produce.
+    import torch
+
+    from paper_2002_00250_b200.pipeline import MultiCameraPipeline
+
+    n, w, h, nf = 3, 48, 32, 26
+    cfgs = {"gmm": PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=3, k_d=3)),
+            "pbas": PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=6), seed=5)}
+    seqs = {name: [synth.sequence("T" if name == "pbas" or shared else "S", w, h, seed=s,
+                                  frames=nf, k_rgb=3) for s in range(n)] for name in cfgs}
+    if shared:
+        seqs["pbas"] = seqs["gmm"]
+    ref = {}
+    for name, cfg in cfgs.items():
+        ref[name] = []
+        for s in range(n):
+            c = PipelineConfig(algorithm=cfg.algorithm, mode="rgbd", gmm=cfg.gmm, pbas=cfg.pbas,
+                               seed=cfg.seed + s)
+            ref[name].append(_run(c, seqs[name][s])[0])
+    with MultiCameraPipeline(cfgs, w, h, n, device=0) as pipe:
+        outs = []
+        for t in range(nf):
+            inp = {name: torch.from_numpy(np.stack([seqs[name][s][t] for s in range(n)])).pin_memory()
+                   for name in cfgs}
+            out = {name: torch.empty((n, h, w), dtype=torch.uint8).pin_memory() for name in cfgs}
+            pipe.submit(inp["gmm"] if shared else inp, out)
+            outs.append(out)
+        pipe.synchronize()
+    for name in cfgs:
+        for s in range(n):
+            got = np.stack([o[name][s].numpy() for o in outs])
+            np.testing.assert_array_equal(got, ref[name][s], err_msg=f"{name} stream {s}")
