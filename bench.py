@@ -256,7 +256,11 @@ def run_ours(args, rank, world, local_rank):
         algos.append(("pbas", p, ring_t, B_ALG.get(("pbas", pbas_n))))
     # One CUDA stream and one mask buffer per algorithm: GMM (HBM-bound) and
     # PBAS (latency-bound K3) are independent engines and run concurrently.
-    streams = {a[0]: torch.cuda.Stream(dev) for a in algos}
+    # PBAS (latency-bound) on a higher-priority stream: the block scheduler
+    # then interleaves its blocks with the bandwidth-bound GMM blocks instead
+    # of draining the whole GMM grid first (--stream-priority 0 disables).
+    prio = {"pbas": -args.stream_priority, "gmm": 0}
+    streams = {a[0]: torch.cuda.Stream(dev, priority=prio[a[0]]) for a in algos}
     masks = {a[0]: torch.empty((S, h, w), dtype=torch.uint8, device=dev) for a in algos}
     main = streams[algos[0][0]]
     torch.cuda.set_stream(main)
@@ -396,8 +400,9 @@ def run_ours(args, rank, world, local_rank):
                        "l2": "inputs larger than L2 (state per step "
                              f"{sum((a[3] or 0) for a in algos) * npix * S / 1e9:.1f} GB >> 126 MB)",
                        "parallelism": f"streams sharded {S}/GPU over {world} GPU(s)",
-                       "schedule": "GMM and PBAS engines on two CUDA streams, concurrently; "
-                                   "per_algo/roofline from a solo phase of each"},
+                       "schedule": "GMM and PBAS engines on two CUDA streams, concurrently "
+                                   f"(PBAS priority +{args.stream_priority}); per_algo/roofline "
+                                   "from a solo phase of each"},
             "fps": fps,
             "per_algo": per_algo,
             "roofline": roof,
@@ -544,6 +549,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
     ap.add_argument("--streams", type=int, default=0, help="override streams per GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--stream-priority", type=int, default=1,
+                    help="PBAS stream priority boost over GMM (0 = equal)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
