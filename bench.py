@@ -549,7 +549,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
     ap.add_argument("--streams", type=int, default=0, help="override streams per GPU")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--stream-priority", type=int, default=1,
+    ap.add_argument("--stream-priority", type=int, default=0,
                     help="PBAS stream priority boost over GMM (0 = equal)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
