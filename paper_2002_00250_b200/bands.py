@@ -92,6 +92,11 @@ class RowBandPbas:
         self._send = torch.empty((2, rb.value), dtype=torch.uint8, device=dev)
         self._recv = torch.empty((2, rb.value), dtype=torch.uint8, device=dev)
         self._L = L
+        self._device_comm = True
+        if world > 1:
+            import torch.distributed as dist
+
+            self._device_comm = dist.get_backend(group) == "nccl"
 
     def step(self, band_frame, band_mask) -> None:
         """Segment this band of one frame (device tensors, (rows, W, 4) and
@@ -113,13 +118,22 @@ class RowBandPbas:
         s0, s1 = self._send[0], self._send[1]
         _native.check(L.rgbdseg_pbas_copy_edges(h, ctypes.c_void_p(s0.data_ptr()),
                                                 ctypes.c_void_p(s1.data_ptr()), st), "copy_edges")
-        works = exchange_intent_halos(s0, s1, self._recv[0], self._recv[1], self.rank,
-                                      self.world, self.group, wait=False)
+        if self._device_comm:
+            works = exchange_intent_halos(s0, s1, self._recv[0], self._recv[1], self.rank,
+                                          self.world, self.group, wait=False)
         if rows > 2:  # interior rows overlap the exchange
             _native.check(L.rgbdseg_pbas_classify_rows(h, fp, mp, 1, rows - 1, st),
                           "classify interior")
-        for w in works:
-            w.wait()
+        if self._device_comm:
+            for w in works:
+                w.wait()
+        else:  # host-staged exchange (gloo: tests that run several ranks on one GPU)
+            import torch
+
+            torch.cuda.current_stream(band_frame.device).synchronize()
+            hs, hr = self._send.cpu(), torch.empty_like(self._send, device="cpu")
+            exchange_intent_halos(hs[0], hs[1], hr[0], hr[1], self.rank, self.world, self.group)
+            self._recv.copy_(hr)
         above = ctypes.c_void_p(self._recv[0].data_ptr()) if self.rank > 0 else None
         below = ctypes.c_void_p(self._recv[1].data_ptr()) if self.rank < self.world - 1 else None
         _native.check(L.rgbdseg_pbas_set_halos(h, above, below, st), "set_halos")

@@ -133,3 +133,59 @@ def make_frame(regime: str, width: int, height: int, seed: int, t: int, k_rgb: i
 
 def sequence(regime: str, width: int, height: int, seed: int, frames: int, k_rgb: int = 7):
     return [make_frame(regime, width, height, seed, t, k_rgb) for t in range(frames)]
+
+
+# ---------------------------------------------------------------------------
+# The reference's acceptance scenes (synth.py:38-160), restated so the
+# acceptance criteria can run on the device path: every frame is a pure
+# function of (spec, t); depth is 16-bit sensor units, GT 0/255.
+# ---------------------------------------------------------------------------
+BG_DEPTH16 = 40000   # synth.py:36
+DEPTH8_UNIT = 257    # synth.py:38
+
+
+class SceneSpec:
+    """SynthSpec (synth.py:41-66) fields used by the scenes below."""
+
+    def __init__(self, scenario, width=160, height=120, frames=160, entry_frame=100,
+                 object_w=40, object_h=40, speed=4, depth_offset=80, colour_offset=90):
+        self.scenario, self.width, self.height, self.frames = scenario, width, height, frames
+        self.entry_frame, self.object_w, self.object_h, self.speed = (entry_frame, object_w,
+                                                                      object_h, speed)
+        self.depth_offset, self.colour_offset = depth_offset, colour_offset
+
+
+def scene_rect(spec: SceneSpec, t: int):
+    """object_rect (synth.py:83-101)."""
+    if spec.scenario in ("static", "illumination_ramp") or t < spec.entry_frame:
+        return None
+    x0 = 4 + spec.speed * (t - spec.entry_frame)
+    if x0 >= spec.width:
+        return None
+    x1 = min(x0 + spec.object_w, spec.width)
+    y0 = max((spec.height - spec.object_h) // 2, 0)
+    y1 = min(y0 + spec.object_h, spec.height)
+    if x1 <= x0 or y1 <= y0:
+        return None
+    return x0, y0, x1, y1
+
+
+def scene_frame(spec: SceneSpec, t: int):
+    """(rgb, depth16, gt) at frame t for static / colour_camouflage /
+    depth_camouflage (synth.py:104-160)."""
+    bg = background_rgb(spec.width, spec.height)
+    rect = scene_rect(spec, t)
+    rgb = bg
+    if spec.scenario == "depth_camouflage" and rect is not None:
+        x0, y0, x1, y1 = rect
+        rgb = bg.copy()
+        region = rgb[y0:y1, x0:x1].astype(np.int32) + spec.colour_offset
+        rgb[y0:y1, x0:x1] = np.clip(region, 0, 255).astype(np.uint8)
+    depth = np.full((spec.height, spec.width), BG_DEPTH16, dtype=np.uint16)
+    gt = np.zeros((spec.height, spec.width), dtype=np.uint8)
+    if rect is not None:
+        x0, y0, x1, y1 = rect
+        if spec.scenario != "depth_camouflage":
+            depth[y0:y1, x0:x1] = BG_DEPTH16 - spec.depth_offset * DEPTH8_UNIT
+        gt[y0:y1, x0:x1] = 255
+    return rgb, depth, gt
