@@ -210,6 +210,12 @@ int rgbdseg_pack_frame(const uint8_t* rgb_dev, int32_t width, int32_t height,
                        const uint16_t* depth16_dev, int32_t depth_w, int32_t depth_h,
                        uint8_t* frame_dev, void* stream);
 
+/* Opt-in 3x3 median postprocess of a 0/255 mask (north_star; no reference
+ * semantics, default off): scipy.ndimage.median_filter(size=3,
+ * mode="reflect") on the device.  Input and output must differ. */
+int rgbdseg_median3x3(const uint8_t* mask_in_dev, uint8_t* mask_out_dev, int32_t width,
+                      int32_t height, void* stream);
+
 /* ---------------------------------------------------- evaluation ------- */
 /* Confusion counts of a device mask against a device ground-truth label
  * plane (0 bg / 1 fg / 2 ignore; frames.py:27-29), accumulated into

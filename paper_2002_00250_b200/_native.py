@@ -31,7 +31,7 @@ EXPORTS = (
     "rgbdseg_pbas_step_batch", "rgbdseg_pbas_process_host", "rgbdseg_pbas_sync",
     "rgbdseg_pbas_get_frame_idx", "rgbdseg_pbas_set_frame_idx", "rgbdseg_pbas_state_bytes",
     "rgbdseg_pbas_read_state", "rgbdseg_pbas_write_state", "rgbdseg_pbas_stream",
-    "rgbdseg_confusion_accumulate", "rgbdseg_pack_frame",
+    "rgbdseg_confusion_accumulate", "rgbdseg_pack_frame", "rgbdseg_median3x3",
 )
 
 GMM_FIELDS = {"rgb_w": 0, "rgb_mu": 1, "rgb_var": 2, "d_w": 3, "d_mu": 4, "d_var": 5}
@@ -100,6 +100,7 @@ def _declare(L):
         "rgbdseg_pbas_stream": (vp, [vp]),
         "rgbdseg_confusion_accumulate": (ctypes.c_int, [vp, vp, i64, vp, vp]),
         "rgbdseg_pack_frame": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, vp, vp]),
+        "rgbdseg_median3x3": (ctypes.c_int, [vp, vp, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -66,3 +66,57 @@ extern "C" int rgbdseg_pack_frame(const uint8_t* rgb_dev, int32_t width, int32_t
     RGBDSEG_LAUNCH_CHECK();
     return RGBDSEG_OK;
 }
+
+// ------------------------------------------------------------------------
+// Opt-in 3x3 median postprocess of a 0/255 mask (north_star "median-filter
+// postprocess"; no reference semantics -- SURVEY.md D4 -- so it is off by
+// default and pinned to scipy.ndimage.median_filter(size=3, mode="reflect")).
+// For a binary mask the median of the 9 values is 255 iff at least 5 are 255.
+// Shared-memory tile with a 1-pixel halo; "reflect" mirrors the edge pixel
+// (index -1 -> 0, W -> W-1).
+namespace rgbdseg {
+constexpr int MED_TX = 32, MED_TY = 8;
+
+__device__ __forceinline__ int reflect_idx(int i, int n) {
+    return i < 0 ? -i - 1 : (i >= n ? 2 * n - i - 1 : i);
+}
+
+__global__ void median3x3_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                 int width, int height) {
+    __shared__ uint8_t tile[MED_TY + 2][MED_TX + 2];
+    const int x0 = blockIdx.x * MED_TX, y0 = blockIdx.y * MED_TY;
+    for (int i = threadIdx.y * MED_TX + threadIdx.x; i < (MED_TY + 2) * (MED_TX + 2);
+         i += MED_TX * MED_TY) {
+        const int ty = i / (MED_TX + 2), tx = i - ty * (MED_TX + 2);
+        const int gy = reflect_idx(min(max(y0 + ty - 1, -1), height), height);
+        const int gx = reflect_idx(min(max(x0 + tx - 1, -1), width), width);
+        tile[ty][tx] = in[(int64_t)gy * width + gx] > 127 ? 1 : 0;
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+    if (x >= width || y >= height) return;
+    int cnt = 0;
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) cnt += tile[threadIdx.y + dy][threadIdx.x + dx];
+    out[(int64_t)y * width + x] = cnt >= 5 ? 255 : 0;
+}
+}  // namespace rgbdseg
+
+extern "C" int rgbdseg_median3x3(const uint8_t* mask_in_dev, uint8_t* mask_out_dev, int32_t width,
+                                 int32_t height, void* stream) {
+    if (!mask_in_dev || !mask_out_dev || mask_in_dev == mask_out_dev) {
+        set_error("median3x3 needs distinct non-NULL input and output masks");
+        return RGBDSEG_E_CONFIG;
+    }
+    if (width <= 0 || height <= 0) {
+        set_error("mask dimensions must be positive");
+        return RGBDSEG_E_DIMENSION;
+    }
+    dim3 block(MED_TX, MED_TY), grid((width + MED_TX - 1) / MED_TX, (height + MED_TY - 1) / MED_TY);
+    median3x3_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(mask_in_dev, mask_out_dev,
+                                                                          width, height);
+    RGBDSEG_LAUNCH_CHECK();
+    return RGBDSEG_OK;
+}

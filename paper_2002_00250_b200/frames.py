@@ -82,3 +82,22 @@ def confusion_counts(mask, labels, device: int = 0):
     _native.check(rc, "confusion_accumulate")
     tp, tn, fp, fn = (int(v) for v in counts.cpu())
     return tp, tn, fp, fn
+
+
+def median3x3(mask, device: int = 0):
+    """Opt-in 3x3 median postprocess of a 0/255 mask (north_star; SURVEY.md D4:
+    not part of the reference, off unless called): equals
+    scipy.ndimage.median_filter(mask, size=3, mode="reflect").  CUDA tensor out."""
+    import torch
+
+    from .engine import torch_stream_handle
+
+    m = _cuda(mask, torch.uint8, device)
+    if m.ndim != 2:
+        raise DimensionError(f"mask must be (H, W), got {tuple(m.shape)}")
+    out = torch.empty_like(m)
+    rc = _native.lib().rgbdseg_median3x3(ctypes.c_void_p(m.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                         int(m.shape[1]), int(m.shape[0]),
+                                         ctypes.c_void_p(torch_stream_handle(m.device)))
+    _native.check(rc, "median3x3")
+    return out

@@ -483,3 +483,13 @@ def test_multicamera_pipeline_matches_single_engines(shared):
         for s in range(n):
             got = np.stack([o[name][s].numpy() for o in outs])
             np.testing.assert_array_equal(got, ref[name][s], err_msg=f"{name} stream {s}")
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (2, 3), (37, 29), (480, 640), (31, 33)])
+def test_median3x3_postprocess_matches_scipy(oracle_mod, shape):
+    # opt-in north_star postprocess; oracle = scipy.ndimage.median_filter
+    from paper_2002_00250_b200.frames import median3x3
+
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    mask = np.where(rng.random(shape) < 0.4, 255, 0).astype(np.uint8)
+    np.testing.assert_array_equal(median3x3(mask).cpu().numpy(), oracle_mod.median3x3(mask))
