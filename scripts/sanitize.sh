@@ -1,0 +1,12 @@
+#!/bin/bash
+# compute-sanitizer memcheck / racecheck / synccheck over small GPU parity cases
+# (every kernel: K1, K2 both intent modes, K3 map + list, pack, median, rng).
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out/sanitizer
+CASES='golden or ragged or row_bands_on_one_gpu or median or pack or confusion or rng or deferred'
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --target-processes all --error-exitcode 9 \
+    python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "$CASES" -p no:cacheprovider \
+    > gpurun_out/sanitizer/$tool.log 2>&1
+  echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|passed|failed' gpurun_out/sanitizer/$tool.log | tail -3 | tr '\n' ' ')"
+done
