@@ -493,3 +493,43 @@ def test_median3x3_postprocess_matches_scipy(oracle_mod, shape):
     rng = np.random.default_rng(shape[0] * 7 + shape[1])
     mask = np.where(rng.random(shape) < 0.4, 255, 0).astype(np.uint8)
     np.testing.assert_array_equal(median3x3(mask).cpu().numpy(), oracle_mod.median3x3(mask))
+
+
+# ------------------------------------------------ C-ABI error paths -------
+def test_capi_error_paths_map_to_reference_exceptions():
+    import ctypes
+
+    import torch
+
+    from paper_2002_00250_b200 import _native
+    from paper_2002_00250_b200.engine import MultiStreamEngine, SegmentationEngine
+    from paper_2002_00250_b200.errors import ConfigError, DimensionError, RgbdSegError
+
+    L = _native.lib()
+    with SegmentationEngine(PipelineConfig(algorithm="gmm"), 8, 6, device=0) as eng:
+        buf = np.empty(10, dtype=np.float64)
+        with pytest.raises(DimensionError):  # wrong byte count for rgb_w (6*8*7 doubles)
+            _native.check(L.rgbdseg_gmm_read_state(eng._h.ptr, 0, buf.ctypes.data, buf.nbytes))
+        with pytest.raises(ConfigError):  # unknown field id
+            _native.check(L.rgbdseg_gmm_read_state(eng._h.ptr, 99, buf.ctypes.data, buf.nbytes))
+        with pytest.raises(DimensionError):
+            eng.load_state({"rgb_w": np.zeros((6, 8, 3))})
+        with pytest.raises(DimensionError):  # process_frame shape check (engine.py:101-105)
+            eng.process_frame(np.zeros((6, 8, 3), dtype=np.uint8))
+    with pytest.raises(ConfigError):  # batch of handles with different parameters
+        a = SegmentationEngine(PipelineConfig(algorithm="gmm", gmm=GmmParams(k_rgb=3)), 8, 6, device=0)
+        b = SegmentationEngine(PipelineConfig(algorithm="gmm", gmm=GmmParams(k_rgb=4)), 8, 6, device=0)
+        hs = (ctypes.c_void_p * 2)(a._h.ptr.value, b._h.ptr.value)
+        fr = torch.zeros((2, 6, 8, 4), dtype=torch.uint8, device="cuda")
+        mk = torch.empty((2, 6, 8), dtype=torch.uint8, device="cuda")
+        fp = (ctypes.c_void_p * 2)(fr[0].data_ptr(), fr[1].data_ptr())
+        mp = (ctypes.c_void_p * 2)(mk[0].data_ptr(), mk[1].data_ptr())
+        _native.check(L.rgbdseg_gmm_step_batch(hs, 2, fp, mp, None))
+    assert issubclass(ConfigError, RgbdSegError)
+    # close() is idempotent
+    eng = SegmentationEngine(PipelineConfig(algorithm="pbas"), 8, 6, device=0)
+    eng.close()
+    eng.close()
+    with pytest.raises(DimensionError):
+        MultiStreamEngine(PipelineConfig(algorithm="gmm"), 8, 6, 2, device=0).process(
+            torch.zeros((3, 6, 8, 4), dtype=torch.uint8, device="cuda"))
