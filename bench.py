@@ -420,8 +420,9 @@ def run_ours(args, rank, world, local_rank):
 
 def run_config5(args, rank, world, local_rank):
     """BASELINE config 5: PBAS on one 7680x4320 stream, row bands across the
-    ranks (engine.py:48-50 split), one-row intent halo over NCCL per frame
-    (bands.RowBandPbas).  value = Mpixel/s of the whole frame."""
+    ranks (engine.py:48-50 split), one-row intent halo per frame through
+    peer-memory mailboxes (bands.RowBandPbas, csrc/peer.cu; --halo nccl for
+    the NCCL send/recv variant).  value = Mpixel/s of the whole frame."""
     import torch
     import torch.distributed as dist
 
@@ -431,7 +432,7 @@ def run_config5(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     w, h, _, _, n = WORKLOADS["config5"]
     cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=n), seed=1)
-    band = RowBandPbas(cfg, w, h, rank, world, device=local_rank)
+    band = RowBandPbas(cfg, w, h, rank, world, device=local_rank, transport=args.halo)
     y0, y1 = band.y0, band.y1
     ring = torch.from_numpy(_gen_ring("T", w, h, [0], 4)[0][:, y0:y1].copy()).to(dev)
     mask = torch.empty((y1 - y0, w), dtype=torch.uint8, device=dev)
@@ -472,7 +473,8 @@ def run_config5(args, rank, world, local_rank):
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8/f64", "data": "synthetic (SURVEY.md §8(d) regime T)",
             "config": {"workload": f"config5: PBAS n={n} on one {w}x{h} RGB-D stream, "
-                                   f"{world} row band(s), 1-row intent halo over NCCL",
+                                   f"{world} row band(s), 1-row intent halo "
+                                   f"({'peer-memory mailboxes' if args.halo == 'p2p' else 'NCCL'})",
                        "width": w, "height": h, "bands": world,
                        "l2": "inputs larger than L2 (PBAS state 4.9 GB)",
                        "parallelism": f"row bands x{world} (engine.py:48-50 split)"},
@@ -481,7 +483,7 @@ def run_config5(args, rank, world, local_rank):
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                          "kernel": "pbas_classify (K2) + pbas_apply (K3), rank 0 band"},
             "cpu_baseline": None, "e2e": None,
-            "gpu_launches": args.steps * (2 if world == 1 else 4),
+            "gpu_launches": args.steps * (2 if world == 1 else 6),
             "clocks": clock_info,
         }
         print(json.dumps(line), flush=True)
@@ -554,6 +556,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
+                    help="config5 row-band intent-halo transport")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -77,6 +77,8 @@ typedef struct rgbdseg_pbas_params {
 
 typedef struct rgbdseg_gmm rgbdseg_gmm;   /* opaque */
 typedef struct rgbdseg_pbas rgbdseg_pbas; /* opaque */
+typedef struct rgbdseg_halo_link rgbdseg_halo_link; /* opaque */
+#define RGBDSEG_IPC_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
 
 /* State field ids; read/write use the reference layout and dtypes. */
 enum {
@@ -188,6 +190,30 @@ int rgbdseg_pbas_set_halos(rgbdseg_pbas* h, const void* above_src, const void* b
  * "no intent" unless the caller fills them between classify and apply. */
 int rgbdseg_pbas_halo_ptrs(rgbdseg_pbas* h, void** first_row, void** last_row, void** halo_above,
                            void** halo_below, int64_t* row_bytes);
+/* Peer-memory halo exchange between row bands on different GPUs (SURVEY.md
+ * §8(e); replaces the reference's in-process band loop, engine.py:126-143,
+ * whose sequential intent phase _apply_intents, pbas.py:511-522, sees every
+ * band's intents).  Each band owns a mailbox in its HBM; neighbours map it
+ * with CUDA IPC (one process per GPU) or directly (same process) and push
+ * their edge intent rows into it with peer stores, synchronised by device
+ * flags -- no host round trip, no NCCL.  Per frame, steps counted from 1:
+ *   classify_rows(edge rows) -> push(step) -> classify_rows(interior)
+ *   -> pull(step) -> apply.
+ * Waits are bounded (default 20 s): a timeout sets an error flag that
+ * status() reports (RGBDSEG_E_RUNTIME) instead of hanging the GPU. */
+int rgbdseg_halo_link_create(rgbdseg_pbas* band, int32_t device, rgbdseg_halo_link** out);
+int rgbdseg_halo_link_export(rgbdseg_halo_link* l, void* ipc_handle_out /* IPC_HANDLE_BYTES */);
+/* Map the neighbours' exported mailboxes (NULL: no band above / below). */
+int rgbdseg_halo_link_connect(rgbdseg_halo_link* l, const void* above_handle,
+                              const void* below_handle);
+/* Same, for neighbour bands owned by this process (same or peer device). */
+int rgbdseg_halo_link_connect_local(rgbdseg_halo_link* l, rgbdseg_halo_link* above,
+                                    rgbdseg_halo_link* below);
+int rgbdseg_halo_link_push(rgbdseg_halo_link* l, uint64_t step, void* stream);
+int rgbdseg_halo_link_pull(rgbdseg_halo_link* l, uint64_t step, void* stream);
+int rgbdseg_halo_link_set_timeout(rgbdseg_halo_link* l, uint64_t timeout_ns);
+int rgbdseg_halo_link_status(rgbdseg_halo_link* l);
+void rgbdseg_halo_link_destroy(rgbdseg_halo_link* l);
 int rgbdseg_pbas_step_batch(rgbdseg_pbas* const* hs, int32_t count,
                             const uint8_t* const* frames_dev, uint8_t* const* masks_dev,
                             void* stream);

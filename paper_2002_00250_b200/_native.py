@@ -32,7 +32,12 @@ EXPORTS = (
     "rgbdseg_pbas_get_frame_idx", "rgbdseg_pbas_set_frame_idx", "rgbdseg_pbas_state_bytes",
     "rgbdseg_pbas_read_state", "rgbdseg_pbas_write_state", "rgbdseg_pbas_stream",
     "rgbdseg_confusion_accumulate", "rgbdseg_pack_frame", "rgbdseg_median3x3",
+    "rgbdseg_halo_link_create", "rgbdseg_halo_link_export", "rgbdseg_halo_link_connect",
+    "rgbdseg_halo_link_connect_local", "rgbdseg_halo_link_push", "rgbdseg_halo_link_pull",
+    "rgbdseg_halo_link_set_timeout", "rgbdseg_halo_link_status", "rgbdseg_halo_link_destroy",
 )
+
+IPC_HANDLE_BYTES = 64  # RGBDSEG_IPC_HANDLE_BYTES
 
 GMM_FIELDS = {"rgb_w": 0, "rgb_mu": 1, "rgb_var": 2, "d_w": 3, "d_mu": 4, "d_var": 5}
 PBAS_FIELDS = {"samples": 0, "dmin_rgb": 1, "dmin_d": 2, "len_rgb": 3, "pos_rgb": 4,
@@ -101,6 +106,15 @@ def _declare(L):
         "rgbdseg_confusion_accumulate": (ctypes.c_int, [vp, vp, i64, vp, vp]),
         "rgbdseg_pack_frame": (ctypes.c_int, [vp, i32, i32, vp, i32, i32, vp, vp]),
         "rgbdseg_median3x3": (ctypes.c_int, [vp, vp, i32, i32, vp]),
+        "rgbdseg_halo_link_create": (ctypes.c_int, [vp, i32, P(vp)]),
+        "rgbdseg_halo_link_export": (ctypes.c_int, [vp, vp]),
+        "rgbdseg_halo_link_connect": (ctypes.c_int, [vp, vp, vp]),
+        "rgbdseg_halo_link_connect_local": (ctypes.c_int, [vp, vp, vp]),
+        "rgbdseg_halo_link_push": (ctypes.c_int, [vp, u64, vp]),
+        "rgbdseg_halo_link_pull": (ctypes.c_int, [vp, u64, vp]),
+        "rgbdseg_halo_link_set_timeout": (ctypes.c_int, [vp, u64]),
+        "rgbdseg_halo_link_status": (ctypes.c_int, [vp]),
+        "rgbdseg_halo_link_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -11,15 +11,24 @@ GPU, torch.distributed for the plumbing):
     (pbas.py:479-507): a band's first/last row may ask a pixel of the
     adjacent band to absorb its own value.  Each band therefore ships ONE row
     of intent codes per boundary per direction (W codes: 7.7 KB at 8K) to the
-    neighbouring rank, which pulls them from its halo rows in K3.
+    neighbouring band, which pulls them from its halo rows in K3.
     Classification reads no neighbour data, so nothing else crosses.
   * The RNG and the in-bounds tests use global (x, y, W, H)
     (rgbdseg_pbas_create_band), so the result is bit-identical to one GPU and
     to the reference for any number of bands.
 
-Per frame, on the current CUDA stream:
-  classify edge rows -> copy them out -> NCCL send/recv (overlaps the
-  interior classify) -> set halos -> K3 pull-apply.
+Transport: peer memory.  Every band owns a mailbox in its
+HBM (csrc/peer.cu); the neighbours map it with CUDA IPC and a one-CTA kernel
+stores the edge rows straight into it over NVLink / NVSwitch, synchronised
+by device flags -- no host round trip and no NCCL on the data path (NCCL
+only reduces the run's counters at the end, bench.py).  Per frame, all on the
+band's CUDA stream:
+
+  classify edge rows -> push (peer stores + ready flag) -> classify interior
+  (overlaps the transfer) -> pull (wait flag, copy into the halo rows,
+  consumed flag) -> K3 pull-apply.
+
+`transport="nccl"` keeps an NCCL send/recv exchange for comparison.
 """
 
 from __future__ import annotations
@@ -72,41 +81,136 @@ def exchange_intent_halos(first_row, last_row, halo_above, halo_below, rank: int
     return works
 
 
+def neighbour_handles(mine: bytes, rank: int, world: int, group=None):
+    """All-gather the bands' mailbox handles (any torch.distributed backend)
+    and return (above, below): the handles of rank-1 and rank+1, None at the
+    frame's top / bottom edge."""
+    import torch.distributed as dist
+
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    return (handles[rank - 1] if rank > 0 else None,
+            handles[rank + 1] if rank < world - 1 else None)
+
+
+class HaloLink:
+    """This band's peer-memory mailbox (rgbdseg_halo_link_*, csrc/peer.cu)."""
+
+    def __init__(self, engine):
+        self._L = _native.lib()
+        self.device = engine.device
+        self._engine = engine  # keeps the band's intent map alive
+        h = ctypes.c_void_p()
+        _native.check(self._L.rgbdseg_halo_link_create(engine._h.ptr, self.device, ctypes.byref(h)),
+                      "halo_link_create")
+        self.ptr = h
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(_native.IPC_HANDLE_BYTES)
+        _native.check(self._L.rgbdseg_halo_link_export(self.ptr, buf), "halo_link_export")
+        return buf.raw
+
+    def connect(self, above: bytes | None, below: bytes | None) -> None:
+        """Map the neighbours' mailboxes (IPC handles from other processes)."""
+        a = ctypes.create_string_buffer(above, len(above)) if above else None
+        b = ctypes.create_string_buffer(below, len(below)) if below else None
+        _native.check(self._L.rgbdseg_halo_link_connect(self.ptr, a, b), "halo_link_connect")
+
+    def connect_local(self, above: "HaloLink | None", below: "HaloLink | None") -> None:
+        """Neighbour bands owned by this process (same or peer device)."""
+        _native.check(self._L.rgbdseg_halo_link_connect_local(
+            self.ptr, above.ptr if above else None, below.ptr if below else None),
+            "halo_link_connect_local")
+
+    def push(self, step: int, stream) -> None:
+        _native.check(self._L.rgbdseg_halo_link_push(self.ptr, step, stream), "halo_link_push")
+
+    def pull(self, step: int, stream) -> None:
+        _native.check(self._L.rgbdseg_halo_link_pull(self.ptr, step, stream), "halo_link_pull")
+
+    def set_timeout(self, seconds: float) -> None:
+        _native.check(self._L.rgbdseg_halo_link_set_timeout(self.ptr, int(seconds * 1e9)),
+                      "halo_link_set_timeout")
+
+    def status(self) -> None:
+        """Synchronise the device and raise DeviceError if a wait timed out."""
+        _native.check(self._L.rgbdseg_halo_link_status(self.ptr), "halo exchange")
+
+    def close(self) -> None:
+        if self.ptr:
+            self._L.rgbdseg_halo_link_destroy(self.ptr)
+            self.ptr = None
+
+
+def band_step_p2p(engine, link, frame, mask, stream) -> None:
+    """One frame of one band with the peer-memory halo exchange (frame and
+    mask: device pointers of the band's rows; stream: cudaStream_t)."""
+    L, h = _native.lib(), engine._h.ptr
+    n = engine.config.pbas.n
+    fidx = engine.frame_idx
+    if fidx < n or link is None:  # warm-up frames emit no intents
+        _native.check(L.rgbdseg_pbas_classify(h, frame, mask, stream), "classify")
+        _native.check(L.rgbdseg_pbas_apply(h, frame, stream), "apply")
+        return
+    step = fidx - n + 1
+    rows = engine.rows
+    _native.check(L.rgbdseg_pbas_classify_rows(h, frame, mask, 0, 1, stream), "classify edge")
+    if rows > 1:
+        _native.check(L.rgbdseg_pbas_classify_rows(h, frame, mask, rows - 1, rows, stream),
+                      "classify edge")
+    link.push(step, stream)
+    if rows > 2:  # interior rows overlap the transfer
+        _native.check(L.rgbdseg_pbas_classify_rows(h, frame, mask, 1, rows - 1, stream),
+                      "classify interior")
+    link.pull(step, stream)
+    _native.check(L.rgbdseg_pbas_apply(h, frame, stream), "apply")
+
+
 class RowBandPbas:
     """This rank's band of a frame split across `world` GPUs (PBAS)."""
 
     def __init__(self, config, width: int, height: int, rank: int, world: int,
-                 device: int | None = None, group=None):
+                 device: int | None = None, group=None, transport: str = "p2p"):
         import torch
 
+        if transport not in ("p2p", "nccl"):
+            raise ValueError(f"transport must be 'p2p' or 'nccl', not {transport!r}")
         self.rank, self.world, self.group = rank, world, group
+        self.transport = transport
         self.y0, self.y1 = band_bounds(height, world)[rank]
         self.engine = SegmentationEngine(config, width, height, device, _band=(self.y0, self.y1))
         self.rows = self.y1 - self.y0
         self.width = width
-        rb = ctypes.c_int64()
-        L = _native.lib()
-        _native.check(L.rgbdseg_pbas_halo_ptrs(self.engine._h.ptr, None, None, None, None,
-                                               ctypes.byref(rb)), "halo_ptrs")
-        dev = torch.device("cuda", self.engine.device)
-        self._send = torch.empty((2, rb.value), dtype=torch.uint8, device=dev)
-        self._recv = torch.empty((2, rb.value), dtype=torch.uint8, device=dev)
-        self._L = L
-        self._device_comm = True
-        if world > 1:
+        self._L = _native.lib()
+        self.link = None
+        if world > 1 and transport == "p2p":
             import torch.distributed as dist
 
-            self._device_comm = dist.get_backend(group) == "nccl"
+            self.link = HaloLink(self.engine)
+            self.link.connect(*neighbour_handles(self.link.export(), rank, world, group))
+            dist.barrier(group)  # every mailbox mapped before the first push
+        elif world > 1:
+            import torch.distributed as dist
+
+            if dist.get_backend(group) != "nccl":
+                raise ValueError("transport='nccl' needs an NCCL process group")
+            rb = ctypes.c_int64()
+            _native.check(self._L.rgbdseg_pbas_halo_ptrs(self.engine._h.ptr, None, None, None,
+                                                         None, ctypes.byref(rb)), "halo_ptrs")
+            dev = torch.device("cuda", self.engine.device)
+            self._send = torch.empty((2, rb.value), dtype=torch.uint8, device=dev)
+            self._recv = torch.empty((2, rb.value), dtype=torch.uint8, device=dev)
 
     def step(self, band_frame, band_mask) -> None:
         """Segment this band of one frame (device tensors, (rows, W, 4) and
         (rows, W) uint8), exchanging the intent halos with the neighbours."""
-        L, h = self._L, self.engine._h.ptr
         st = ctypes.c_void_p(torch_stream_handle(band_frame.device))
         fp, mp = ctypes.c_void_p(band_frame.data_ptr()), ctypes.c_void_p(band_mask.data_ptr())
-        n = self.engine.config.pbas.n
-        if self.engine.frame_idx < n or self.world == 1:
-            # warm-up frames emit no intents; a single band has no neighbour
+        if self.world == 1 or self.transport == "p2p":
+            band_step_p2p(self.engine, self.link, fp, mp, st)
+            return
+        L, h = self._L, self.engine._h.ptr
+        if self.engine.frame_idx < self.engine.config.pbas.n:
             _native.check(L.rgbdseg_pbas_classify(h, fp, mp, st), "classify")
             _native.check(L.rgbdseg_pbas_apply(h, fp, st), "apply")
             return
@@ -118,26 +222,25 @@ class RowBandPbas:
         s0, s1 = self._send[0], self._send[1]
         _native.check(L.rgbdseg_pbas_copy_edges(h, ctypes.c_void_p(s0.data_ptr()),
                                                 ctypes.c_void_p(s1.data_ptr()), st), "copy_edges")
-        if self._device_comm:
-            works = exchange_intent_halos(s0, s1, self._recv[0], self._recv[1], self.rank,
-                                          self.world, self.group, wait=False)
+        works = exchange_intent_halos(s0, s1, self._recv[0], self._recv[1], self.rank,
+                                      self.world, self.group, wait=False)
         if rows > 2:  # interior rows overlap the exchange
             _native.check(L.rgbdseg_pbas_classify_rows(h, fp, mp, 1, rows - 1, st),
                           "classify interior")
-        if self._device_comm:
-            for w in works:
-                w.wait()
-        else:  # host-staged exchange (gloo: tests that run several ranks on one GPU)
-            import torch
-
-            torch.cuda.current_stream(band_frame.device).synchronize()
-            hs, hr = self._send.cpu(), torch.empty_like(self._send, device="cpu")
-            exchange_intent_halos(hs[0], hs[1], hr[0], hr[1], self.rank, self.world, self.group)
-            self._recv.copy_(hr)
+        for w in works:
+            w.wait()
         above = ctypes.c_void_p(self._recv[0].data_ptr()) if self.rank > 0 else None
         below = ctypes.c_void_p(self._recv[1].data_ptr()) if self.rank < self.world - 1 else None
         _native.check(L.rgbdseg_pbas_set_halos(h, above, below, st), "set_halos")
         _native.check(L.rgbdseg_pbas_apply(h, fp, st), "apply")
 
+    def status(self) -> None:
+        """Raise if a peer-memory wait timed out (synchronises the device)."""
+        if self.link is not None:
+            self.link.status()
+
     def close(self):
+        if self.link is not None:
+            self.link.close()
+            self.link = None
         self.engine.close()

@@ -118,3 +118,35 @@ def test_band_bounds_match_reference_linspace():
     assert band_bounds(10, 3) == [(0, 3), (3, 6), (6, 10)]
     assert band_bounds(4320, 8)[-1] == (3780, 4320)
     assert band_bounds(3, 8)[0] == (0, 0)  # more bands than rows: empty bands (test_engine.py:120-127)
+
+
+def _handles_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+
+    from paper_2002_00250_b200.bands import neighbour_handles
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = bytes([rank]) * 64  # stands in for a cudaIpcMemHandle_t
+    got = neighbour_handles(mine, rank, world)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, got)
+    if rank == 0:
+        np.save(out_path, np.array(gathered, dtype=object), allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_link_handles_go_to_adjacent_bands(tmp_path, world):
+    # bands.RowBandPbas maps rank-1's mailbox as "above" and rank+1's as
+    # "below" (the band order of engine.py:48-50); the frame edges get None
+    import torch.multiprocessing as mp
+
+    out = tmp_path / "handles.npy"
+    mp.start_processes(_handles_worker, args=(world, _free_port(), str(out)), nprocs=world,
+                       start_method="spawn", join=True)
+    got = np.load(out, allow_pickle=True)
+    for r, (above, below) in enumerate(got):
+        assert above == (bytes([r - 1]) * 64 if r > 0 else None)
+        assert below == (bytes([r + 1]) * 64 if r < world - 1 else None)
