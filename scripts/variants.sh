@@ -2,6 +2,7 @@
 # Benchmark tuning variants of the native library (tuning/lib_*.so) on the GPU box.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
+shopt -s nullglob
 for lib in "" tuning/lib_*.so; do
   tag=${lib:-default}; tag=$(basename "$tag" .so)
   RGBDSEG_B200_LIB=${lib:+$PWD/$lib} timeout 300 python bench.py --steps 60 --warmup 10 --no-e2e --no-cpu-baseline ${VARIANT_BENCH_ARGS} > gpurun_out/var_$tag.json 2> gpurun_out/var_$tag.err

@@ -176,3 +176,22 @@ def test_oracle_pack_frame_matches_reference(oracle_mod):
     for tag in ("all", "up", "odd", "down", "p720_480"):
         np.testing.assert_array_equal(oracle_mod.pack_frame(fx[f"{tag}_rgb"], fx[f"{tag}_d16"]),
                                       fx[f"{tag}_frame"], err_msg=tag)
+
+
+def test_markstein_ratio_exhaustive(tmp_path):
+    # K2's ratio() (csrc/pbas.cu) replaces the IEEE divide tot / len of the
+    # dmin averages (pbas.py:432, :448) by a Markstein step with RN(1/n):
+    # exact for every (tot, len) the state can hold.
+    import shutil
+    import subprocess
+    from pathlib import Path
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    src = Path(__file__).parent / "native" / "markstein_ratio.c"
+    exe = tmp_path / "markstein_ratio"
+    subprocess.run([cc, "-O2", "-ffp-contract=off", "-o", str(exe), str(src), "-lm"], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout
+    assert "cases 16711680 mismatches 0" in r.stdout
