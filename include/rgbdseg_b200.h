@@ -227,6 +227,12 @@ int rgbdseg_pbas_read_state(rgbdseg_pbas* h, int32_t field, void* host_dst, int6
 int rgbdseg_pbas_write_state(rgbdseg_pbas* h, int32_t field, const void* host_src, int64_t bytes);
 void* rgbdseg_pbas_stream(rgbdseg_pbas* h);
 
+/* Device self-test of K2's divide without the IEEE slow-path branch
+ * (csrc/pbas.cu fdiv_rn) against `/`: *mismatches = number of i with
+ * bitwise-different quotients a_dev[i] / b_dev[i] (synchronous). */
+int rgbdseg_selftest_fdiv(const double* a_dev, const double* b_dev, int64_t n,
+                          int64_t* mismatches);
+
 /* ------------------------------------------------- input staging ------ */
 /* frames.scale_depth_map + resample_depth + pack_frame (src/rgbdseg/frames.py:46-88)
  * on the device: rgb (H,W,3) u8 and depth16 (depth_h, depth_w) u16 (nearest-

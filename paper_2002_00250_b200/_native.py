@@ -35,6 +35,7 @@ EXPORTS = (
     "rgbdseg_halo_link_create", "rgbdseg_halo_link_export", "rgbdseg_halo_link_connect",
     "rgbdseg_halo_link_connect_local", "rgbdseg_halo_link_push", "rgbdseg_halo_link_pull",
     "rgbdseg_halo_link_set_timeout", "rgbdseg_halo_link_status", "rgbdseg_halo_link_destroy",
+    "rgbdseg_selftest_fdiv",
 )
 
 IPC_HANDLE_BYTES = 64  # RGBDSEG_IPC_HANDLE_BYTES
@@ -115,6 +116,7 @@ def _declare(L):
         "rgbdseg_halo_link_set_timeout": (ctypes.c_int, [vp, u64]),
         "rgbdseg_halo_link_status": (ctypes.c_int, [vp]),
         "rgbdseg_halo_link_destroy": (None, [vp]),
+        "rgbdseg_selftest_fdiv": (ctypes.c_int, [vp, vp, i64, P(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -533,3 +533,44 @@ def test_capi_error_paths_map_to_reference_exceptions():
     with pytest.raises(DimensionError):
         MultiStreamEngine(PipelineConfig(algorithm="gmm"), 8, 6, 2, device=0).process(
             torch.zeros((3, 6, 8, 4), dtype=torch.uint8, device="cuda"))
+
+
+def test_fast_divide_matches_ieee_divide_on_device():
+    # K2's fdiv_rn (csrc/pbas.cu) = the div.rn.f64 fast path without its
+    # slow-path branch, used only for operands the host proved in range.
+    # Bitwise against `/` on the device over the operand families K2 feeds
+    # it (pbas.py:432/448 averages, :462/:464 T steps, :468 1/T, :474/:486
+    # u/prob) plus log-uniform pairs across the whole accepted range.
+    import ctypes
+
+    import torch
+
+    from paper_2002_00250_b200 import _native
+
+    L = _native.lib()
+    rng = np.random.default_rng(7)
+    m = 4_000_000
+
+    def check(a, b, what):
+        ad = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+        bd = torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).cuda()
+        bad = ctypes.c_int64(-1)
+        _native.check(L.rgbdseg_selftest_fdiv(ctypes.c_void_p(ad.data_ptr()),
+                                              ctypes.c_void_p(bd.data_ptr()), ad.numel(),
+                                              ctypes.byref(bad)))
+        assert bad.value == 0, f"{what}: {bad.value} mismatches"
+
+    tot, ln = np.meshgrid(np.arange(65536.0), np.arange(1.0, 256.0))
+    check(tot.ravel(), ln.ravel(), "tot/len exhaustive")
+    tt = rng.uniform(2.0, 200.0, m)
+    check(np.ones(m), tt, "1/T")
+    prob = 1.0 / tt
+    u = rng.integers(0, 2**53, m).astype(np.float64) * 2.0**-53
+    check(u * prob, prob, "u/prob (u < prob)")
+    check(u, prob, "u/prob")
+    guard = rng.uniform(1.0, 255.0, m)
+    num = np.where(rng.random(m) < 0.5, 1.0, -0.05) * 10.0 ** rng.uniform(-3, 3, m)
+    check(num, guard, "t_step/guard")
+    a = 10.0 ** rng.uniform(-145, 145, m) * np.where(rng.random(m) < 0.5, 1.0, -1.0)
+    b = 10.0 ** rng.uniform(-145, 145, m)
+    check(a, b, "log-uniform")
