@@ -137,8 +137,10 @@ def test_gmm_component_counts(oracle_mod, k_rgb, k_d, mode):
     _compare_with_oracle(oracle_mod, cfg, frames, gu.GMM_KEYS, exact_masks=False)
 
 
-@pytest.mark.parametrize("n,mm", [(1, 1), (20, 20), (31, 2), (32, 3), (64, 2), (255, 4)])
+@pytest.mark.parametrize("n,mm", [(1, 1), (2, 2), (7, 1), (20, 1), (20, 3), (20, 20), (31, 2),
+                                  (32, 3), (64, 2), (255, 4)])
 def test_pbas_buffer_sizes(oracle_mod, n, mm):
+    # (20, 1/2): pair scan; (20, 3): counters; other n: runtime-n scans
     # n > 31 switches the intent map to 16-bit codes.
     frames = synth.sequence("T", 40, 24, seed=6, frames=n + 25)
     cfg = PipelineConfig(algorithm="pbas", pbas=PbasParams(n=n, min_matches=mm), seed=n)
@@ -574,3 +576,46 @@ def test_fast_divide_matches_ieee_divide_on_device():
     a = 10.0 ** rng.uniform(-145, 145, m) * np.where(rng.random(m) < 0.5, 1.0, -1.0)
     b = 10.0 ** rng.uniform(-145, 145, m)
     check(a, b, "log-uniform")
+
+
+@pytest.mark.parametrize("r", [0.5, 300.0])
+def test_pbas_extreme_radius_thresholds(oracle_mod, r):
+    # R < 1: only exact matches count (threshold 1); R > 255: every RGB
+    # distance and every valid depth counts (threshold 256, pbas.py:392,
+    # :413) -- the edges of the order-statistic scans
+    frames = synth.sequence("T", 48, 20, seed=3, frames=40)
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", seed=5,
+                         pbas=PbasParams(n=20, r_init=r, r_lower=r))
+    _compare_with_oracle(oracle_mod, cfg, frames, gu.PBAS_KEYS, exact_masks=True)
+
+
+@pytest.mark.parametrize("w,h", [(64, 37), (96, 8), (32, 1), (640, 480)])
+def test_pbas_list_handle_row_ranges(oracle_mod, w, h):
+    # A single-band (intent-list) handle classified in uneven row ranges
+    # (classify_rows) before one apply: intents across a range boundary must
+    # land exactly as in the reference's whole-frame pass.
+    import ctypes
+
+    import torch
+
+    from paper_2002_00250_b200 import _native
+    from paper_2002_00250_b200.engine import SegmentationEngine, torch_stream_handle
+
+    n = 6
+    frames = synth.sequence("T", w, h, seed=17, frames=n + 20)
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=n), seed=29)
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    cuts = sorted({0, h, min(h, 5), min(h, 13), h // 2})
+    L = _native.lib()
+    st = ctypes.c_void_p(torch_stream_handle())
+    with SegmentationEngine(cfg, w, h, device=0) as eng:
+        for t, f in enumerate(frames):
+            fr = torch.from_numpy(f).cuda()
+            mask = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+            fp, mp = ctypes.c_void_p(fr.data_ptr()), ctypes.c_void_p(mask.data_ptr())
+            for r0, r1 in zip(cuts[:-1], cuts[1:]):
+                _native.check(L.rgbdseg_pbas_classify_rows(eng._h.ptr, fp, mp, r0, r1, st))
+            _native.check(L.rgbdseg_pbas_apply(eng._h.ptr, fp, st))
+            np.testing.assert_array_equal(mask.cpu().numpy(), ref.process_frame(f), err_msg=f"frame {t}")
+        got = {k: v.copy() for k, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
