@@ -233,6 +233,21 @@ void* rgbdseg_pbas_stream(rgbdseg_pbas* h);
 int rgbdseg_selftest_fdiv(const double* a_dev, const double* b_dev, int64_t n,
                           int64_t* mismatches);
 
+/* Fused evaluation epilogue: metrics.compare_masks (src/rgbdseg/metrics.py:50-69)
+ * inside K1/K2.  set_eval(h, labels_dev) makes the following steps compare
+ * each pixel's decision with labels_dev (H*W u8 of the handle's rows:
+ * 0 background, 1 foreground, 2 ignore; frames.py:27-29) and accumulate
+ * TP/TN/FP/FN on the device; NULL turns it off.  eval_counts writes (or with
+ * accumulate=1 adds) the pooled counts {tp, tn, fp, fn} (aggregate_sequence's
+ * pooling, metrics.py:89-101) into counts_dev[4] (int64, device) on `stream`
+ * and, with reset=1, restarts the pool.  Stream-ordered, no host sync. */
+int rgbdseg_gmm_set_eval(rgbdseg_gmm* h, const uint8_t* labels_dev);
+int rgbdseg_gmm_eval_counts(rgbdseg_gmm* h, int64_t* counts_dev, int32_t accumulate, int32_t reset,
+                            void* stream);
+int rgbdseg_pbas_set_eval(rgbdseg_pbas* h, const uint8_t* labels_dev);
+int rgbdseg_pbas_eval_counts(rgbdseg_pbas* h, int64_t* counts_dev, int32_t accumulate,
+                             int32_t reset, void* stream);
+
 /* ------------------------------------------------- input staging ------ */
 /* frames.scale_depth_map + resample_depth + pack_frame (src/rgbdseg/frames.py:46-88)
  * on the device: rgb (H,W,3) u8 and depth16 (depth_h, depth_w) u16 (nearest-

@@ -35,7 +35,8 @@ EXPORTS = (
     "rgbdseg_halo_link_create", "rgbdseg_halo_link_export", "rgbdseg_halo_link_connect",
     "rgbdseg_halo_link_connect_local", "rgbdseg_halo_link_push", "rgbdseg_halo_link_pull",
     "rgbdseg_halo_link_set_timeout", "rgbdseg_halo_link_status", "rgbdseg_halo_link_destroy",
-    "rgbdseg_selftest_fdiv",
+    "rgbdseg_selftest_fdiv", "rgbdseg_gmm_set_eval", "rgbdseg_gmm_eval_counts",
+    "rgbdseg_pbas_set_eval", "rgbdseg_pbas_eval_counts",
 )
 
 IPC_HANDLE_BYTES = 64  # RGBDSEG_IPC_HANDLE_BYTES
@@ -117,6 +118,10 @@ def _declare(L):
         "rgbdseg_halo_link_status": (ctypes.c_int, [vp]),
         "rgbdseg_halo_link_destroy": (None, [vp]),
         "rgbdseg_selftest_fdiv": (ctypes.c_int, [vp, vp, i64, P(i64)]),
+        "rgbdseg_gmm_set_eval": (ctypes.c_int, [vp, vp]),
+        "rgbdseg_gmm_eval_counts": (ctypes.c_int, [vp, vp, i32, i32, vp]),
+        "rgbdseg_pbas_set_eval": (ctypes.c_int, [vp, vp]),
+        "rgbdseg_pbas_eval_counts": (ctypes.c_int, [vp, vp, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

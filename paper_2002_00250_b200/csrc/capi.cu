@@ -64,6 +64,28 @@ __global__ void confusion_kernel(const uint8_t* __restrict__ mask,
     }
 }
 
+__global__ void eval_sum_kernel(unsigned long long* __restrict__ slots,
+                                long long* __restrict__ counts, int accumulate, int reset) {
+    // one warp per counter: lanes stride over the slots, then a warp sum
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long v = 0;
+    for (int i = lane; i < EVAL_SLOTS; i += 32) {
+        v += slots[i * 4 + c];
+        if (reset) slots[i * 4 + c] = 0ull;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) counts[c] = (accumulate ? counts[c] : 0ll) + (long long)v;
+}
+
+int eval_sum_slots(unsigned long long* slots, int64_t* counts_dev, int accumulate, int reset,
+                   cudaStream_t st) {
+    eval_sum_kernel<<<1, 128, 0, st>>>(slots, reinterpret_cast<long long*>(counts_dev), accumulate,
+                                       reset);
+    RGBDSEG_LAUNCH_CHECK();
+    return RGBDSEG_OK;
+}
+
 }  // namespace rgbdseg
 
 using namespace rgbdseg;

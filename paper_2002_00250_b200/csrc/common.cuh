@@ -49,6 +49,44 @@ struct DeviceGuard {
     }
 };
 
+// ------------------------------------------- fused evaluation epilogue --
+// metrics.compare_masks (src/rgbdseg/metrics.py:50-69) folded into K1/K2:
+// fg = this pixel's mask decision, label 0 background / 1 foreground /
+// 2 ignore (frames.py:27-29; ignore counts nowhere).  Ballot + popc per
+// warp, shared-memory sums per block, one 64-bit atomic per counter per
+// block into one of EVAL_SLOTS spread slots (no hot address); the slots
+// are summed by rgbdseg_eval_sum_slots.  Every thread of the block must call
+// it (it synchronises the block).
+constexpr int EVAL_SLOTS = 256;
+
+__device__ __forceinline__ void eval_block_accumulate(bool valid, bool fg, uint8_t label,
+                                                      unsigned long long* __restrict__ slots) {
+    __shared__ unsigned int sc[4];
+    if (threadIdx.x < 4) sc[threadIdx.x] = 0u;
+    __syncthreads();
+    const bool fgl = valid && label == 1, bgl = valid && label == 0;
+    const unsigned tp = __ballot_sync(0xFFFFFFFFu, fg && fgl);
+    const unsigned tn = __ballot_sync(0xFFFFFFFFu, !fg && bgl);
+    const unsigned fp = __ballot_sync(0xFFFFFFFFu, fg && bgl);
+    const unsigned fn = __ballot_sync(0xFFFFFFFFu, !fg && fgl);
+    if ((threadIdx.x & 31u) == 0) {
+        if (tp) atomicAdd(&sc[0], (unsigned)__popc(tp));
+        if (tn) atomicAdd(&sc[1], (unsigned)__popc(tn));
+        if (fp) atomicAdd(&sc[2], (unsigned)__popc(fp));
+        if (fn) atomicAdd(&sc[3], (unsigned)__popc(fn));
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && sc[threadIdx.x])
+        atomicAdd(slots + (size_t)(blockIdx.x & (EVAL_SLOTS - 1)) * 4 + threadIdx.x,
+                  (unsigned long long)sc[threadIdx.x]);
+}
+
+// Sum the EVAL_SLOTS x 4 slot counters into counts[4] (device, stream-
+// ordered; counts += sum when accumulate, else counts = sum) and optionally
+// zero the slots.  Defined in capi.cu.
+int eval_sum_slots(unsigned long long* slots, int64_t* counts_dev, int accumulate, int reset,
+                   cudaStream_t st);
+
 // Round a plane length up so every plane of 8/16/32-byte records starts on a
 // 256-byte boundary (full-sector, 256-bit-load friendly).
 inline int64_t plane_pitch(int64_t npix) { return (npix + 31) / 32 * 32; }

@@ -216,9 +216,16 @@ class SegmentationEngine:
                 f"({self.rows}, {self.width}, 4)"
             )
 
-    def process_frame(self, frame):
-        """Segment one packed (H, W, 4) uint8 frame; returns the 0/255 mask."""
+    def process_frame(self, frame, labels=None):
+        """Segment one packed (H, W, 4) uint8 frame; returns the 0/255 mask.
+
+        labels: optional ground truth for this frame ((H, W) uint8, 0 bg /
+        1 fg / 2 ignore, frames.py:27-29, or a GroundTruthMask): the kernel
+        counts TP/TN/FP/FN as it writes the mask (metrics.compare_masks fused
+        into K1/K2), pooled on the device -- read with confusion_counts()."""
         self._check_shape(frame.shape)
+        if labels is not None:
+            return self._process_eval(frame, labels)
         if _is_torch(frame) and frame.is_cuda:
             return self._process_device(frame)
         if _is_torch(frame):
@@ -269,6 +276,51 @@ class SegmentationEngine:
         stream = torch_stream_handle(frame.device)
         self.step_device(frame.data_ptr(), mask.data_ptr(), stream)
         return mask
+
+    def _process_eval(self, frame, labels):
+        import torch
+
+        from .metrics import _labels_of
+
+        host = not (_is_torch(frame) and frame.is_cuda)
+        dev = torch.device("cuda", self.device)
+        lab = _labels_of(labels)
+        lab = lab if _is_torch(lab) else torch.from_numpy(np.ascontiguousarray(lab, dtype=np.uint8))
+        if tuple(lab.shape) != (self.rows, self.width):
+            raise DimensionError(f"mask dimensions {(self.rows, self.width)} do not match ground "
+                                 f"truth {tuple(lab.shape)}")  # metrics.py:57-60
+        lab = lab.to(device=dev, dtype=torch.uint8).contiguous()
+        fr = frame if not host else torch.from_numpy(
+            np.ascontiguousarray(frame.numpy() if _is_torch(frame) else frame, dtype=np.uint8))
+        fr = fr.to(dev)
+        _native.check(self._h.fn("set_eval")(self._h.ptr, ctypes.c_void_p(lab.data_ptr())),
+                      "set_eval")
+        try:
+            mask = self._process_device(fr)
+        finally:
+            self._h.fn("set_eval")(self._h.ptr, None)
+        self._eval_keep = lab  # alive until the stream has consumed it
+        return mask.cpu().numpy() if host else mask
+
+    def confusion_counts_device(self, out=None, reset: bool = False):
+        """The pooled (tp, tn, fp, fn) of every frame processed with labels
+        since the last reset, as a CUDA int64[4] tensor written on the current
+        stream (no host sync; feed it to metrics.all_reduce_counts)."""
+        import torch
+
+        if out is None:
+            out = torch.empty(4, dtype=torch.int64, device=torch.device("cuda", self.device))
+        rc = self._h.fn("eval_counts")(self._h.ptr, ctypes.c_void_p(out.data_ptr()), 0, int(reset),
+                                       ctypes.c_void_p(torch_stream_handle(out.device)))
+        _native.check(rc, "eval_counts")
+        return out
+
+    def confusion_counts(self, reset: bool = False):
+        """Pooled ConfusionCounts of the frames processed with labels
+        (metrics.aggregate_sequence's pooling, metrics.py:94-101)."""
+        from .metrics import ConfusionCounts
+
+        return ConfusionCounts.from_sequence(self.confusion_counts_device(reset=reset).tolist())
 
     def step_device(self, frame_ptr: int, mask_ptr: int, stream: int = 0) -> None:
         """Raw device-pointer step (frame/mask already in HBM)."""
@@ -343,11 +395,21 @@ class MultiStreamEngine:
         self._fn = (_native.lib().rgbdseg_gmm_step_batch if config.algorithm == "gmm"
                     else _native.lib().rgbdseg_pbas_step_batch)
 
-    def step_ptrs(self, frame_ptrs, mask_ptrs, stream: int = 0) -> None:
+    def step_ptrs(self, frame_ptrs, mask_ptrs, stream: int = 0, label_ptrs=None) -> None:
+        """One batched frame; label_ptrs (device pointers of per-stream
+        ground-truth planes, or None) turns on the fused confusion counts."""
         for i in range(self.n):
             self._fr[i] = frame_ptrs[i]
             self._mk[i] = mask_ptrs[i]
-        rc = self._fn(self._hs, self.n, self._fr, self._mk, ctypes.c_void_p(stream))
+        if label_ptrs is not None:
+            for e, lp in zip(self.engines, label_ptrs):
+                _native.check(e._h.fn("set_eval")(e._h.ptr, ctypes.c_void_p(lp)), "set_eval")
+        try:
+            rc = self._fn(self._hs, self.n, self._fr, self._mk, ctypes.c_void_p(stream))
+        finally:
+            if label_ptrs is not None:
+                for e in self.engines:
+                    e._h.fn("set_eval")(e._h.ptr, None)
         _native.check(rc, "step_batch")
         for e in self.engines:
             e._gmm_frame_idx += 1

@@ -619,3 +619,75 @@ def test_pbas_list_handle_row_ranges(oracle_mod, w, h):
             np.testing.assert_array_equal(mask.cpu().numpy(), ref.process_frame(f), err_msg=f"frame {t}")
         got = {k: v.copy() for k, v in eng.state_arrays().items()}
     _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
+
+
+def _labels_seq(frames, seed):
+    rng = np.random.default_rng(seed)
+    return [rng.choice(3, size=f.shape[:2], p=[0.5, 0.35, 0.15]).astype(np.uint8) for f in frames]
+
+
+def _counts_oracle(mask, labels):  # metrics.compare_masks, metrics.py:50-69
+    fg = mask > 127
+    return (int(np.count_nonzero(fg & (labels == 1))), int(np.count_nonzero(~fg & (labels == 0))),
+            int(np.count_nonzero(fg & (labels == 0))), int(np.count_nonzero(~fg & (labels == 1))))
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_fused_confusion_counts_pool_like_aggregate_sequence(oracle_mod, algo):
+    # process_frame(frame, labels) counts TP/TN/FP/FN inside K1/K2; the pool
+    # must equal summing compare_masks over the frames (aggregate_sequence),
+    # while masks and state stay bit-exact with the unevaluated run.
+    from paper_2002_00250_b200.errors import DimensionError
+    from paper_2002_00250_b200.metrics import ConfusionCounts, aggregate_sequence, compute_metrics
+
+    w, h = 67, 29  # ragged: partial warps/blocks
+    frames = synth.sequence("T", w, h, seed=5, frames=30)
+    labels = _labels_seq(frames, 9)
+    cfg = (PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=3, k_d=3))
+           if algo == "gmm" else PipelineConfig(algorithm="pbas", mode="rgbd",
+                                                pbas=PbasParams(n=8), seed=4))
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    want = ConfusionCounts()
+    with _engine(cfg, w, h) as eng:
+        for t, (f, lab) in enumerate(zip(frames, labels)):
+            m = eng.process_frame(f, labels=lab)
+            m_ref = ref.process_frame(f)
+            np.testing.assert_array_equal(m, m_ref, err_msg=f"frame {t}")
+            want = want + ConfusionCounts(*_counts_oracle(m_ref, lab))
+            if t == 10:
+                assert eng.confusion_counts() == want
+        assert eng.confusion_counts(reset=True) == want
+        assert aggregate_sequence([want]) == compute_metrics(eng_counts := want)
+        assert eng.confusion_counts() == ConfusionCounts()  # pool restarted
+        with pytest.raises(DimensionError):
+            eng.process_frame(frames[0], labels=labels[0][:, :-1])
+        got = {k: v.copy() for k, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), gu.GMM_KEYS if algo == "gmm" else gu.PBAS_KEYS)
+    assert eng_counts.total == sum(int(np.count_nonzero(l != 2)) for l in labels)
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_fused_confusion_counts_batched_streams(algo):
+    import torch
+
+    from paper_2002_00250_b200.engine import MultiStreamEngine, torch_stream_handle
+    from paper_2002_00250_b200.metrics import ConfusionCounts
+
+    w, h, S = 96, 40, 3
+    seqs = [synth.sequence("T", w, h, seed=20 + i, frames=12) for i in range(S)]
+    labs = [_labels_seq(seq, 30 + i) for i, seq in enumerate(seqs)]
+    cfg = (PipelineConfig(algorithm="gmm", mode="rgbd") if algo == "gmm"
+           else PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=6), seed=2))
+    want = [ConfusionCounts() for _ in range(S)]
+    with MultiStreamEngine(cfg, w, h, S, device=0) as ms:
+        for t in range(12):
+            fr = torch.from_numpy(np.stack([seqs[i][t] for i in range(S)])).cuda()
+            lb = torch.from_numpy(np.stack([labs[i][t] for i in range(S)])).cuda()
+            masks = torch.empty((S, h, w), dtype=torch.uint8, device="cuda")
+            ms.step_ptrs([fr[i].data_ptr() for i in range(S)], [masks[i].data_ptr() for i in range(S)],
+                         torch_stream_handle(), label_ptrs=[lb[i].data_ptr() for i in range(S)])
+            mh = masks.cpu().numpy()
+            for i in range(S):
+                want[i] = want[i] + ConfusionCounts(*_counts_oracle(mh[i], labs[i][t]))
+        for i in range(S):
+            assert ms.engines[i].confusion_counts() == want[i], f"stream {i}"
