@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/rgbdseg_b200.h"
 
@@ -86,6 +87,42 @@ __device__ __forceinline__ void eval_block_accumulate(bool valid, bool fg, uint8
 // zero the slots.  Defined in capi.cu.
 int eval_sum_slots(unsigned long long* slots, int64_t* counts_dev, int accumulate, int reset,
                    cudaStream_t st);
+
+// ------------------------------------------ programmatic dependent launch --
+// K1, K2 and K3 are launched with programmatic stream serialisation: the
+// next kernel of the stream (the next frame's K1, K3 after K2, the next
+// frame's K2 after K3) is scheduled into the SMs the previous one's tail
+// frees, and waits on the device (griddepcontrol.wait = the previous grid
+// completed and its memory is visible) instead of paying a full launch gap.
+// Every kernel launched this way calls pdl_enter() before touching memory.
+#ifndef RGBDSEG_PDL
+#define RGBDSEG_PDL 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if RGBDSEG_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st,
+                       Args&&... args) {
+#if RGBDSEG_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+#else
+    kern<<<grid, block, 0, st>>>(std::forward<Args>(args)...);
+#endif
+}
 
 // Round a plane length up so every plane of 8/16/32-byte records starts on a
 // 256-byte boundary (full-sector, 256-bit-load friendly).
