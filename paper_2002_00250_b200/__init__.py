@@ -24,6 +24,9 @@ _LAZY = {
     "MultiStreamEngine": ("engine", "MultiStreamEngine"),
     "pixel_rng": ("rng", "pixel_rng"),
     "rng_stream": ("rng", "rng_stream"),
+    "process_sequence": ("sequence", "process_sequence"),
+    "RunStats": ("sequence", "RunStats"),
+    "MemorySequence": ("sequence", "MemorySequence"),
 }
 
 
@@ -38,6 +41,7 @@ def __getattr__(name):
 
 __all__ = [
     "GmmParams", "PbasParams", "PipelineConfig", "SegmentationEngine", "MultiStreamEngine",
-    "pixel_rng", "rng_stream", "RgbdSegError", "DimensionError", "FormatError",
+    "pixel_rng", "rng_stream", "process_sequence", "RunStats", "MemorySequence", "RgbdSegError",
+    "DimensionError", "FormatError",
     "SequenceError", "ConfigError", "DeviceError", "__version__",
 ]

@@ -237,6 +237,13 @@ class SegmentationEngine:
         self._gmm_frame_idx += 1
         return mask
 
+    def pack(self, rgb, depth16=None):
+        """frames.pack_frame (+ resample_depth when the depth size differs,
+        frames.py:46-88) on this engine's device: a CUDA (H, W, 4) frame."""
+        from .frames import pack_frame
+
+        return pack_frame(rgb, depth16, device=self.device)
+
     def apply(self, rgb, depth16=None):
         """apply(rgb, depth) -> mask (the north_star's segmenter call): packs
         RGB + 16-bit depth on the device (frames.py:46-88; depth resampled

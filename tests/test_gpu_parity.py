@@ -691,3 +691,49 @@ def test_fused_confusion_counts_batched_streams(algo):
                 want[i] = want[i] + ConfusionCounts(*_counts_oracle(mh[i], labs[i][t]))
         for i in range(S):
             assert ms.engines[i].confusion_counts() == want[i], f"stream {i}"
+
+
+@pytest.mark.parametrize("algo,mode", [("gmm", "rgbd"), ("pbas", "rgbd"), ("pbas", "rgb_only")])
+def test_process_sequence_matches_reference_pipeline(oracle_mod, algo, mode):
+    # engine.py:146-214: resample (depth at another size) + pack + segment per
+    # frame; masks to on_mask; labels -> pooled metrics (aggregate_sequence)
+    from paper_2002_00250_b200.errors import SequenceError
+    from paper_2002_00250_b200.metrics import ConfusionCounts, aggregate_sequence
+    from paper_2002_00250_b200.sequence import MemorySequence, process_sequence
+
+    w, h, n = 64, 48, 26
+    rng = np.random.default_rng(3)
+    base = rng.integers(0, 256, (h, w, 3), dtype=np.uint8)
+    rgbs, deps, labs = [], [], []
+    for t in range(n):
+        img = base.copy()
+        img[10:20, (t % 40):(t % 40) + 12] = 200  # a moving block
+        rgbs.append(img)
+        d = np.full((h // 2, w // 2), 40000, np.uint16)  # half-size depth: resampled
+        d[rng.random(d.shape) < 0.05] = 0
+        deps.append(d)
+        lab = np.zeros((h, w), np.uint8)
+        lab[10:20, (t % 40):(t % 40) + 12] = 1
+        lab[0, :] = 2
+        labs.append(lab)
+    src = MemorySequence(rgbs, deps if mode == "rgbd" else None)
+    cfg = (PipelineConfig(algorithm="gmm", mode=mode) if algo == "gmm"
+           else PipelineConfig(algorithm="pbas", mode=mode, pbas=PbasParams(n=6), seed=11))
+    got = []
+    stats = process_sequence(src, cfg, on_mask=lambda fid, m: got.append((fid, m.copy())),
+                             labels=labs)
+    assert stats.frames_processed == n and len(stats.per_frame_seconds) == n
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    want = ConfusionCounts()
+    for t in range(n):
+        frame = oracle_mod.pack_frame(rgbs[t], oracle_mod.resample_depth(deps[t], w, h)
+                                      if mode == "rgbd" else None)
+        m = ref.process_frame(frame)
+        assert got[t][0] == src.frame_id(t)
+        if algo == "pbas":
+            np.testing.assert_array_equal(got[t][1], m, err_msg=f"frame {t}")
+        want = want + ConfusionCounts(*_counts_oracle(got[t][1], labs[t]))
+    assert stats.report == aggregate_sequence([want])
+    bad = MemorySequence(rgbs[:2] + [rgbs[2][:, :-1]], deps[:3] if mode == "rgbd" else None)
+    with pytest.raises(SequenceError, match="differ"):
+        process_sequence(bad, cfg)

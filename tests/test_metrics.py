@@ -89,3 +89,21 @@ def test_all_reduce_counts_sums_rank_pools(tmp_path):
     mp.start_processes(_reduce_worker, args=(3, _port(), str(out)), nprocs=3, start_method="spawn",
                        join=True)
     assert np.load(out).tolist() == [6, 30, 6, 0]
+
+
+def test_process_sequence_validates_like_reference():
+    # engine.py:158-162: empty sequence and rgbd without depth fail before
+    # any device work
+    from paper_2002_00250_b200.config import PipelineConfig
+    from paper_2002_00250_b200.errors import SequenceError
+    from paper_2002_00250_b200.sequence import MemorySequence, RunStats, process_sequence
+
+    with pytest.raises(SequenceError, match="empty"):
+        process_sequence(MemorySequence([]), PipelineConfig(algorithm="gmm"))
+    rgb = [np.zeros((4, 4, 3), np.uint8)]
+    with pytest.raises(SequenceError, match="depth"):
+        process_sequence(MemorySequence(rgb), PipelineConfig(algorithm="gmm", mode="rgbd"))
+    with pytest.raises(SequenceError, match="length"):
+        MemorySequence(rgb, depth16=[])
+    st = RunStats(frames_processed=4, seconds=2.0)
+    assert st.fps == 2.0 and st.seconds_per_frame == 0.5
