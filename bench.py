@@ -137,6 +137,18 @@ def _gen_ring(regime, w, h, seeds, ring, k_rgb=7):
 
 
 # --------------------------------------------------------- CPU baseline ----
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_sample(w, h, gmm_k, pbas_n, seed, budget_s=12.0, max_frames=400, workers=None):
     """Time the oracle port (reference algorithm, CPU) on a bounded sample:
     one w x h stream, GMM + PBAS per frame, after an untimed burn-in."""
@@ -219,6 +231,7 @@ def run_reference_arm(args, rank, world):
                    "gmm": list(gmm_k) if gmm_k else None, "pbas_n": pbas_n},
         "fps": args.steps / dt,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "cpu_model": _cpu_model(),
                          "sample": f"{args.steps} timed steps x one {w}x{h} frame (GMM+PBAS), "
                                    f"oracle/ C port of the reference numba kernels, {workers} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -416,6 +429,12 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_sample(w, h, gmm_k, pbas_n, seed=0, budget_s=args.cpu_budget)
+            # also one core, and name the CPU
+            one = cpu_sample(w, h, gmm_k, pbas_n, seed=0, budget_s=max(2.0, args.cpu_budget / 4),
+                             max_frames=40, workers=1)
+            cpu["value_1_core"] = one["value"]
+            cpu["sample_1_core"] = one["sample"]
+            cpu["cpu_model"] = _cpu_model()
         except Exception as exc:  # report, never fail the bench line
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port",
                    "sample": f"failed: {exc}"}
