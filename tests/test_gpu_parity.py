@@ -737,3 +737,20 @@ def test_process_sequence_matches_reference_pipeline(oracle_mod, algo, mode):
     bad = MemorySequence(rgbs[:2] + [rgbs[2][:, :-1]], deps[:3] if mode == "rgbd" else None)
     with pytest.raises(SequenceError, match="differ"):
         process_sequence(bad, cfg)
+
+
+def test_pbas_load_state_rejects_positions_outside_the_ring():
+    # pos must stay < n and len <= n (pbas.py:425-431); the reference's ring
+    # write would leave its buffer otherwise -- rejected like bad config
+    from paper_2002_00250_b200.errors import ConfigError
+
+    cfg = PipelineConfig(algorithm="pbas", pbas=PbasParams(n=5), seed=1)
+    with _engine(cfg, 16, 8) as eng:
+        for key, bad in (("pos_rgb", 5), ("pos_d", 200), ("len_rgb", 6)):
+            st = eng.state_arrays()[key].copy()
+            st[3, 4] = bad
+            with pytest.raises(ConfigError):
+                eng.load_state({key: st})
+        ok = eng.state_arrays()["len_d"].copy()
+        ok[:] = 5
+        eng.load_state({"len_d": ok})
