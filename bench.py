@@ -562,7 +562,7 @@ def run_e2e(args, algos, S, w, h, dev, world):
     from paper_2002_00250_b200.pipeline import MultiCameraPipeline
 
     npix = w * h
-    steps = max(3, min(args.steps, args.e2e_steps))
+    steps = max(3, args.e2e_steps)  # pipeline fill + drain amortised over the steps
     pipe = MultiCameraPipeline({}, w, h, S, device=dev.index, engines={a[0]: a[1] for a in algos})
     host_in = {}
     for name, eng, ring, _ in algos:
@@ -611,7 +611,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--stream-priority", type=int, default=0,
                     help="PBAS stream priority boost over GMM (0 = equal)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
