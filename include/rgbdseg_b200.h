@@ -214,6 +214,14 @@ int rgbdseg_halo_link_pull(rgbdseg_halo_link* l, uint64_t step, void* stream);
 int rgbdseg_halo_link_set_timeout(rgbdseg_halo_link* l, uint64_t timeout_ns);
 int rgbdseg_halo_link_status(rgbdseg_halo_link* l);
 void rgbdseg_halo_link_destroy(rgbdseg_halo_link* l);
+/* K2 variant (performance only; every variant gives the same result):
+ * 0 auto (default) -- the row kernel while few pixels emit neighbour updates,
+ * the 32x8 tile kernel (in-tile updates applied inside K2) once many do, chosen
+ * from the update count K3 posts each frame; 1 always rows; 2 always tiles
+ * (tiles need a single-band handle with width % 32 == 0).  get returns the
+ * variant the next step will use (1 rows, 2 tiles). */
+int rgbdseg_pbas_set_k2_mode(rgbdseg_pbas* h, int32_t mode);
+int32_t rgbdseg_pbas_get_k2_mode(const rgbdseg_pbas* h);
 int rgbdseg_pbas_step_batch(rgbdseg_pbas* const* hs, int32_t count,
                             const uint8_t* const* frames_dev, uint8_t* const* masks_dev,
                             void* stream);

@@ -36,7 +36,8 @@ EXPORTS = (
     "rgbdseg_halo_link_connect_local", "rgbdseg_halo_link_push", "rgbdseg_halo_link_pull",
     "rgbdseg_halo_link_set_timeout", "rgbdseg_halo_link_status", "rgbdseg_halo_link_destroy",
     "rgbdseg_selftest_fdiv", "rgbdseg_gmm_set_eval", "rgbdseg_gmm_eval_counts",
-    "rgbdseg_pbas_set_eval", "rgbdseg_pbas_eval_counts",
+    "rgbdseg_pbas_set_eval", "rgbdseg_pbas_eval_counts", "rgbdseg_pbas_set_k2_mode",
+    "rgbdseg_pbas_get_k2_mode",
 )
 
 IPC_HANDLE_BYTES = 64  # RGBDSEG_IPC_HANDLE_BYTES
@@ -122,6 +123,8 @@ def _declare(L):
         "rgbdseg_gmm_eval_counts": (ctypes.c_int, [vp, vp, i32, i32, vp]),
         "rgbdseg_pbas_set_eval": (ctypes.c_int, [vp, vp]),
         "rgbdseg_pbas_eval_counts": (ctypes.c_int, [vp, vp, i32, i32, vp]),
+        "rgbdseg_pbas_set_k2_mode": (ctypes.c_int, [vp, i32]),
+        "rgbdseg_pbas_get_k2_mode": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -754,3 +754,30 @@ def test_pbas_load_state_rejects_positions_outside_the_ring():
         ok = eng.state_arrays()["len_d"].copy()
         ok[:] = 5
         eng.load_state({"len_d": ok})
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_pbas_k2_variants_and_auto_switch(oracle_mod, mode):
+    # K2 runs as the row kernel or as the 32x8 tile kernel that applies
+    # in-tile neighbour updates itself; auto mode switches on the update
+    # rate K3 posts.  A fast T decay (t_dec) drives the rate from ~1/18 to
+    # 1/2 within the sequence, so auto mode must cross over -- every frame
+    # bit-exact with the reference in every mode.
+    from paper_2002_00250_b200 import _native
+
+    w, h, n = 96, 40, 6
+    frames = synth.sequence("T", w, h, seed=12, frames=70)
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", seed=5,
+                         pbas=PbasParams(n=n, t_dec=1.0, t_lower=2.0))
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    L = _native.lib()
+    seen = set()
+    with _engine(cfg, w, h) as eng:
+        _native.check(L.rgbdseg_pbas_set_k2_mode(eng._h.ptr, mode))
+        for t, f in enumerate(frames):
+            seen.add(int(L.rgbdseg_pbas_get_k2_mode(eng._h.ptr)))
+            np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
+                                          err_msg=f"frame {t}")
+        got = {k: v.copy() for k, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
+    assert seen == ({1, 2} if mode == 0 else {mode})
