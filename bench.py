@@ -425,6 +425,17 @@ def run_ours(args, rank, world, local_rank):
             "peak_kind": peak_kind,
             "bytes_per_launch_alg": (per_algo[dom]["bytes_per_pixel_alg"] or 0) * npix * S}
 
+    # PBAS's per-frame work grows with model age (update probability 1/T, T
+    # adapting down, DESIGN.md): report the timed frame window and T then.
+    age_info = {"timed_frames": [t_frame_by[algos[0][0]] - args.steps, t_frame_by[algos[0][0]]]}
+    for name, eng, _, _ in algos:
+        if name == "pbas":
+            import numpy as np
+
+            tt = eng.engines[0].state_arrays()["t"]
+            age_info.update({"pbas_T_median": float(np.median(tt)),
+                             "pbas_k2_variant": ("tiles" if _native_k2_mode(eng) == 2 else "rows")})
+
     # ---- e2e through the public host-buffer API (rank-local, then max)
     e2e = None
     if not args.no_e2e:
@@ -445,16 +456,6 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port",
                    "sample": f"failed: {exc}"}
 
-    # PBAS's per-frame work grows with model age (update probability 1/T, T
-    # adapting down, DESIGN.md): report the timed frame window and T then.
-    age_info = {"timed_frames": [t_frame_by[algos[0][0]] - args.steps, t_frame_by[algos[0][0]]]}
-    for name, eng, _, _ in algos:
-        if name == "pbas":
-            import numpy as np
-
-            tt = eng.engines[0].state_arrays()["t"]
-            age_info.update({"pbas_T_median": float(np.median(tt)),
-                             "pbas_k2_variant": ("tiles" if _native_k2_mode(eng) == 2 else "rows")})
     if rank == 0:
         wl_desc = (f"{args.workload}: {S} x {w}x{h} RGB-D streams per GPU"
                    + (f", GMM {gmm_k[0]}/{gmm_k[1]} (regime S)" if gmm_k else "")
