@@ -647,6 +647,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: several ranks on ONE GPU (gloo plumbing, same device for all)
+    # to exercise the multi-rank bench logic on a single-GPU box
+    shared = os.environ.get("RGBDSEG_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local_rank = 0
 
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
@@ -656,7 +661,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         if args.workload == "config5":
             return run_config5(args, rank, world, local_rank)
