@@ -4,8 +4,9 @@ peer-memory intent-halo exchange (csrc/peer.cu):
   * 2 and 3 ranks over gloo, all on cuda:0: each rank maps its neighbours'
     mailboxes with CUDA IPC (the multi-GPU code path; on one device the
     "peer" stores land in the same HBM) and synchronises with device flags;
-  * 2 and 3 bands in ONE process (connect_local), including several frames
-    in flight on one stream;
+  * 2, 3, 4 and 8 bands in ONE process (connect_local), including several
+    frames in flight on one stream, and 8 bands of a 1080p frame against one
+    band and the CPU reference;
   * a neighbour that never pushes: the bounded wait reports DeviceError
     instead of hanging the GPU.
 
@@ -90,7 +91,7 @@ def test_row_band_pbas_ranks_ipc_match_single_engine(oracle_mod, tmp_path, world
             np.testing.assert_array_equal(v, ref.state_arrays()[k][y0:y1], err_msg=f"{k} {y0}:{y1}")
 
 
-@pytest.mark.parametrize("nbands", [2, 3])
+@pytest.mark.parametrize("nbands", [2, 3, 4, 8])
 def test_row_bands_local_peer_links_match_oracle(oracle_mod, nbands):
     # All bands in one process on one device, mailboxes connected directly;
     # every band's frame is enqueued on ONE stream in band order, so a band's
@@ -168,4 +169,56 @@ def test_halo_wait_times_out_instead_of_hanging():
     for l in links:
         l.close()
     for e in engines:
+        e.close()
+
+
+def test_eight_bands_1080p_match_one_band_and_oracle(oracle_mod):
+    # a frame split into 8 row bands (the 8-GPU layout, here
+    # 8 handles on one device linked through their peer-memory mailboxes)
+    # must equal one band and the CPU reference bit for bit, at full HD with
+    # the paper's n = 20 (30 frames: 20 warm-up + 10 with neighbour updates).
+    import torch
+
+    from paper_2002_00250_b200 import _native
+    from paper_2002_00250_b200.bands import HaloLink, band_bounds
+    from paper_2002_00250_b200.engine import SegmentationEngine, torch_stream_handle
+
+    w, h, nb = 1920, 1080, 8
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=20), seed=77)
+    frames = synth.sequence("T", w, h, seed=2, frames=30)
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    one = SegmentationEngine(cfg, w, h, device=0)
+    bounds = band_bounds(h, nb)
+    engines = [SegmentationEngine(cfg, w, h, device=0, _band=b) for b in bounds]
+    links = [HaloLink(e) for e in engines]
+    for i, l in enumerate(links):
+        l.connect_local(links[i - 1] if i > 0 else None, links[i + 1] if i < nb - 1 else None)
+    L = _native.lib()
+    st = ctypes.c_void_p(torch_stream_handle())
+    for t, f in enumerate(frames):
+        fr = torch.from_numpy(f).cuda()
+        mask = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+        ptrs = [(ctypes.c_void_p(fr[y0:y1].data_ptr()), ctypes.c_void_p(mask[y0:y1].data_ptr()))
+                for (y0, y1) in bounds]
+        step = t - cfg.pbas.n + 1
+        for e, l, (fp, mp) in zip(engines, links, ptrs):
+            _native.check(L.rgbdseg_pbas_classify_rows(e._h.ptr, fp, mp, 0, e.rows, st))
+            if step >= 1:
+                l.push(step, st)
+        for e, l, (fp, _) in zip(engines, links, ptrs):
+            if step >= 1:
+                l.pull(step, st)
+            _native.check(L.rgbdseg_pbas_apply(e._h.ptr, fp, st))
+        want = one.process_frame(fr).cpu().numpy()
+        np.testing.assert_array_equal(mask.cpu().numpy(), want, err_msg=f"frame {t}")
+        np.testing.assert_array_equal(want, ref.process_frame(f), err_msg=f"frame {t} vs oracle")
+    for l in links:
+        l.status()
+    for k, v in one.state_arrays().items():
+        np.testing.assert_array_equal(v, ref.state_arrays()[k], err_msg=k)
+        np.testing.assert_array_equal(
+            np.concatenate([e.state_arrays()[k] for e in engines]), v, err_msg=f"bands {k}")
+    for l in links:
+        l.close()
+    for e in engines + [one]:
         e.close()
