@@ -16,10 +16,15 @@ ranks per second, each pixel segmented by both algorithms); weak scaling
 Inputs: SURVEY.md §8(d) regimes, generated untimed and uploaded to HBM as a
 frame ring per stream: GMM runs on regime S (every component seeded, so the
 algorithmic byte count is honest), PBAS on regime T (moving objects + depth
-holes).  The state is burned in to steady state before the warm-up steps
-(GMM: all 7/3 components seeded; PBAS: 2n = 40 frames, dmin rings full).
+holes).  The state is burned in before the warm-up steps (GMM: all 7/3
+components seeded; PBAS: 2n = 40 frames, dmin rings full).
+With the default --warmup 10 --steps 100 the timed frames are 100-200 of the
+200-frame BASELINE config-4 sequence.  PBAS's work per frame keeps growing
+with model age (update probability 1/T, T adapting down), so the
+line reports the timed window, T's median and the K2 variant (`model_age`).
 The per-step working set (5.8 GB GMM + 2.5 GB PBAS state per GPU) is far
-larger than L2, so no explicit flush is needed.
+larger than L2, so no explicit flush is needed; smaller workloads (configs
+1-2) flush L2 between individually timed steps.
 
 Extra keys: roofline (GMM K1, the dominant kernel), per-algorithm breakdown,
 cpu_baseline (the oracle port on this host's cores), e2e (the public
