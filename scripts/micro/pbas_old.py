@@ -17,6 +17,11 @@ eng = MultiStreamEngine(PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasP
 ring = torch.from_numpy(_gen_ring("T", w, h, list(range(S)), 8)).to(dev)
 masks = torch.empty((S, h, w), dtype=torch.uint8, device=dev)
 R, npix, st = ring.shape[1], w * h, torch_stream_handle(dev)
+if "tiles" in sys.argv[2:]:  # pin the tile K2 (profilers replay kernels; auto mode reads host memory)
+    from paper_2002_00250_b200 import _native
+
+    for e in eng.engines:
+        _native.check(_native.lib().rgbdseg_pbas_set_k2_mode(e._h.ptr, 2))
 for t in range(frames + 5):
     eng.step_ptrs([ring.data_ptr() + ((i * R) + (t % R)) * npix * 4 for i in range(S)],
                   [masks.data_ptr() + i * npix for i in range(S)], st)
