@@ -70,7 +70,7 @@ def _loader(source):
     if hasattr(source, "load"):
         return source.load
     try:  # a reference SequenceSource on disk: read it with the reference's own I/O
-        from rgbdseg import frame_io  # noqa: PLC0415
+        from rgbdseg import frames as frame_io  # the reference engine.py:23 alias
     except ImportError as exc:  # pragma: no cover - depends on the caller's environment
         raise SequenceError("source has no load(i) and rgbdseg.frame_io is not importable") from exc
 
