@@ -72,7 +72,7 @@ def _loader(source):
     try:  # a reference SequenceSource on disk: read it with the reference's own I/O
         from rgbdseg import frames as frame_io  # the reference engine.py:23 alias
     except ImportError as exc:  # pragma: no cover - depends on the caller's environment
-        raise SequenceError("source has no load(i) and rgbdseg.frame_io is not importable") from exc
+        raise SequenceError("source has no load(i) and rgbdseg.frames is not importable") from exc
 
     def load(i):
         rgb = frame_io.load_rgb(source.rgb_paths[i])
@@ -101,6 +101,19 @@ def process_sequence(source, config, on_mask: Optional[Callable] = None, labels=
     if labels is not None and len(labels) != len(source):
         raise SequenceError("labels must cover every frame of the sequence")
     load = _loader(source)
+    out_dir, write_png = None, None
+    if getattr(config, "emit_masks", False):  # engine.py:165-171; PNG writing is the reference's
+        if config.out_dir is None:
+            raise SequenceError("emit_masks is set but no out_dir configured")
+        try:
+            from rgbdseg import frames as frame_io  # noqa: PLC0415
+        except ImportError as exc:
+            raise SequenceError("emit_masks needs the reference's rgbdseg.frames (PNG I/O)") from exc
+        from pathlib import Path
+
+        out_dir = Path(config.out_dir)
+        out_dir.mkdir(parents=True, exist_ok=True)
+        write_png = frame_io.write_mask_png
     stats = RunStats()
     engine = None
     try:
@@ -127,6 +140,8 @@ def process_sequence(source, config, on_mask: Optional[Callable] = None, labels=
             stats.frames_processed += 1
             stats.seconds += dt
             stats.per_frame_seconds.append(dt)
+            if out_dir is not None:
+                write_png(out_dir / f"{source.frame_id(i)}.png", mask)
             if on_mask is not None:
                 on_mask(source.frame_id(i), mask)
         if labels is not None:
