@@ -105,5 +105,8 @@ def test_process_sequence_validates_like_reference():
         process_sequence(MemorySequence(rgb), PipelineConfig(algorithm="gmm", mode="rgbd"))
     with pytest.raises(SequenceError, match="length"):
         MemorySequence(rgb, depth16=[])
+    with pytest.raises(SequenceError, match="out_dir"):
+        process_sequence(MemorySequence(rgb), PipelineConfig(algorithm="gmm", mode="rgb_only",
+                                                             emit_masks=True))
     st = RunStats(frames_processed=4, seconds=2.0)
     assert st.fps == 2.0 and st.seconds_per_frame == 0.5
