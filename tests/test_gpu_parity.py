@@ -781,3 +781,24 @@ def test_pbas_k2_variants_and_auto_switch(oracle_mod, mode):
         got = {k: v.copy() for k, v in eng.state_arrays().items()}
     _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
     assert seen == ({1, 2} if mode == 0 else {mode})
+
+
+@pytest.mark.parametrize("n,mm,mode", [(40, 2, "rgbd"), (7, 3, "rgbd"), (20, 1, "rgb_only"),
+                                       (20, 2, "rgbd")])
+def test_pbas_tile_variant_code_widths_and_scans(oracle_mod, n, mm, mode):
+    # the pinned tile K2 with 16-bit codes (n > 31), the counter scan
+    # (min_matches > 2), rgb_only, and the paper's n = 20, against the reference
+    from paper_2002_00250_b200 import _native
+
+    w, h = 64, 24
+    frames = synth.sequence("T", w, h, seed=31, frames=n + 15)
+    cfg = PipelineConfig(algorithm="pbas", mode=mode, seed=9,
+                         pbas=PbasParams(n=n, min_matches=mm, t_dec=0.5))
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=1)
+    with _engine(cfg, w, h) as eng:
+        _native.check(_native.lib().rgbdseg_pbas_set_k2_mode(eng._h.ptr, 2))
+        for t, f in enumerate(frames):
+            np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
+                                          err_msg=f"frame {t}")
+        got = {k: v.copy() for k, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
