@@ -432,7 +432,8 @@ def run_ours(args, rank, world, local_rank):
 
     # PBAS's per-frame work grows with model age (update probability 1/T, T
     # adapting down): report the timed frame window and T then.
-    age_info = {"timed_frames": [t_frame_by[algos[0][0]] - args.steps, t_frame_by[algos[0][0]]]}
+    done = int(algos[0][1].engines[0].frame_idx)  # frames each engine has segmented
+    age_info = {"timed_frames": [done - args.steps, done]}
     for name, eng, _, _ in algos:
         if name == "pbas":
             import numpy as np
