@@ -89,5 +89,23 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: Path | No
     return lib_out
 
 
+def build_capi_demo(verbose: bool = False) -> Path:
+    """examples/capi_demo: a plain C host of the C-ABI (no Python), linked
+    against the in-tree library (rpath $ORIGIN/../paper_2002_00250_b200)."""
+    src = ROOT / "examples" / "capi_demo.c"
+    out = ROOT / "examples" / "capi_demo"
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        raise RuntimeError("no C compiler for examples/capi_demo.c")
+    cmd = [cc, "-O2", "-std=c11", "-Wall", "-Wextra", "-o", str(out), str(src),
+           "-L", str(PKG), "-lrgbdseg_b200", "-Wl,-rpath,$ORIGIN/../paper_2002_00250_b200"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"capi_demo build failed:\n{r.stderr}")
+    if verbose:
+        print(f"built {out}", file=sys.stderr)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)

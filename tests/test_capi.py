@@ -123,3 +123,34 @@ def test_magic_division_used_for_pixel_rows():
         ns = [0, 1, d - 1, d, d + 1, 2 ** 31 - 1] + [int(v) for v in rng.integers(0, 2 ** 31, 20)]
         for n in ns:
             assert _udiv(n, d) == n // d, (n, d)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_plain_c_host_matches_python_engine(tmp_path, algo):
+    # examples/capi_demo.c drives the path through the C-ABI alone (the
+    # boundary a non-Python host binds); its masks and state must equal the
+    # Python engine's on the same frames, bit for bit.
+    import subprocess
+
+    import numpy as np
+
+    from paper_2002_00250_b200 import _build
+    from paper_2002_00250_b200.config import GmmParams, PbasParams, PipelineConfig
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    exe = _build.build_capi_demo()
+    w, h, n, seed = 64, 48, 30, 7
+    out = tmp_path / "demo.bin"
+    subprocess.run([str(exe), algo, str(w), str(h), str(n), str(seed), str(out)], check=True)
+    raw = np.fromfile(out, dtype=np.uint8)
+    frames = raw[: n * h * w * 4].reshape(n, h, w, 4)
+    masks = raw[n * h * w * 4: n * h * w * 5].reshape(n, h, w)
+    state = raw[n * h * w * 5:].view(np.float64)
+    cfg = (PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams()) if algo == "gmm" else
+           PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(), seed=seed + 1))
+    with SegmentationEngine(cfg, w, h, device=0) as eng:
+        for t in range(n):
+            np.testing.assert_array_equal(eng.process_frame(frames[t]), masks[t], err_msg=f"frame {t}")
+        key = "rgb_w" if algo == "gmm" else "r_rgb"
+        np.testing.assert_array_equal(eng.state_arrays()[key].ravel(), state)
