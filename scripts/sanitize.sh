@@ -4,7 +4,7 @@
 # pack, median, rng, fast divide self-test, peer-memory halo push/pull).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out/sanitizer
-CASES='golden or ragged or row_bands_on_one_gpu or median or pack or confusion or rng or deferred or list_handle or fast_divide or process_sequence or extreme'
+CASES='golden or ragged or row_bands_on_one_gpu or median or pack or confusion or rng or deferred or list_handle or fast_divide or process_sequence or extreme or k2_variants or tile_variant'
 for tool in memcheck racecheck synccheck; do
   timeout 1500 compute-sanitizer --tool $tool --target-processes all --error-exitcode 9 \
     python -m pytest tests/test_gpu_parity.py tests/test_gpu_bands.py -m gpu -q -x \
