@@ -9,6 +9,8 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/rgbdseg_b200.h"
 
 namespace rgbdseg {
@@ -87,6 +89,15 @@ __device__ __forceinline__ void eval_block_accumulate(bool valid, bool fg, uint8
 // zero the slots.  Defined in capi.cu.
 int eval_sum_slots(unsigned long long* slots, int64_t* counts_dev, int accumulate, int reset,
                    cudaStream_t st);
+
+// ------------------------------------------------------------- tracing --
+// NVTX range around every C-ABI step (SURVEY.md §5 "tracing"): what an
+// nsys / ncu --nvtx capture of a host application groups the K1/K2/K3
+// launches under.  Header-only NVTX3: a pointer test when no tool attaches.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------ programmatic dependent launch --
 // K1, K2 and K3 are launched with programmatic stream serialisation: the

@@ -311,6 +311,7 @@ int rgbdseg_halo_link_push(rgbdseg_halo_link* l, uint64_t step, void* stream) {
     }
     if (!l->above && !l->below) return RGBDSEG_OK;
     DeviceGuard dg(l->device);
+    NvtxRange nvtx("rgbdseg.halo_push");
     halo_push_kernel<<<1, 512, 0, static_cast<cudaStream_t>(stream)>>>(args_of(l, step));
     RGBDSEG_LAUNCH_CHECK();
     return RGBDSEG_OK;
@@ -323,6 +324,7 @@ int rgbdseg_halo_link_pull(rgbdseg_halo_link* l, uint64_t step, void* stream) {
     }
     if (!l->above && !l->below) return RGBDSEG_OK;
     DeviceGuard dg(l->device);
+    NvtxRange nvtx("rgbdseg.halo_pull");
     halo_pull_kernel<<<1, 512, 0, static_cast<cudaStream_t>(stream)>>>(args_of(l, step));
     RGBDSEG_LAUNCH_CHECK();
     return RGBDSEG_OK;
