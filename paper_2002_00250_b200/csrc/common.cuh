@@ -94,9 +94,16 @@ int eval_sum_slots(unsigned long long* slots, int64_t* counts_dev, int accumulat
 // NVTX range around every C-ABI step (SURVEY.md §5 "tracing"): what an
 // nsys / ncu --nvtx capture of a host application groups the K1/K2/K3
 // launches under.  Header-only NVTX3: a pointer test when no tool attaches.
+#ifndef RGBDSEG_NVTX
+#define RGBDSEG_NVTX 1
+#endif
 struct NvtxRange {
+#if RGBDSEG_NVTX
     explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
     ~NvtxRange() { nvtxRangePop(); }
+#else
+    explicit NvtxRange(const char*) {}
+#endif
 };
 
 // ------------------------------------------ programmatic dependent launch --
