@@ -99,7 +99,11 @@ enum {
     RGBDSEG_PBAS_POS_D = 6,    /* (H,W)     u8  pbas.py:291 */
     RGBDSEG_PBAS_R_RGB = 7,    /* (H,W)     f64 pbas.py:292 */
     RGBDSEG_PBAS_R_D = 8,      /* (H,W)     f64 pbas.py:293 */
-    RGBDSEG_PBAS_T = 9         /* (H,W)     f64 pbas.py:294 */
+    RGBDSEG_PBAS_T = 9,        /* (H,W)     f64 pbas.py:294 */
+    /* opt-in gradient feature only (rgbdseg_pbas_set_gradient; no reference
+     * counterpart): */
+    RGBDSEG_PBAS_GSAMPLES = 10,  /* (H,W,n) u8  gradient magnitude of every sample */
+    RGBDSEG_PBAS_GRAD_PREV = 11  /* ()      u64 previous frame's magnitude sum (~0: none) */
 };
 
 /* ------------------------------------------------------------ common ---- */
@@ -214,6 +218,15 @@ int rgbdseg_halo_link_pull(rgbdseg_halo_link* l, uint64_t step, void* stream);
 int rgbdseg_halo_link_set_timeout(rgbdseg_halo_link* l, uint64_t timeout_ns);
 int rgbdseg_halo_link_status(rgbdseg_halo_link* l);
 void rgbdseg_halo_link_destroy(rgbdseg_halo_link* l);
+/* Opt-in PBAS gradient-magnitude feature (no reference counterpart: the
+ * reference drops the original PBAS gradient term; semantics in
+ * DESIGN.md §3 "K2G", CPU checker oracle_pbas_frame_g).  Switched before the
+ * first frame of a single-band handle: enable = 1 with alpha >= 0 (sample
+ * distance dist + alpha / max(mean g of the previous frame, 1) * |g - g_i|)
+ * and mean_init > 0 (the mean before the first frame); enable = 0 returns to
+ * the reference algorithm.  Adds state fields RGBDSEG_PBAS_GSAMPLES and
+ * RGBDSEG_PBAS_GRAD_PREV. */
+int rgbdseg_pbas_set_gradient(rgbdseg_pbas* h, int32_t enable, double alpha, double mean_init);
 /* K2 variant (performance only; every variant gives the same result):
  * 0 auto (default) -- the row kernel while few pixels emit neighbour updates,
  * the 32x8 tile kernel (in-tile updates applied inside K2) once many do, chosen

@@ -58,6 +58,11 @@ def lib():
     L.oracle_pbas_frame.restype = i64
     L.oracle_pbas_frame.argtypes = ([i64, i64, vp, i64] + [vp] * 10 + [u64, i32, i32]
                                     + [f64] * 7 + [i32, vp, i32])
+    L.oracle_pbas_frame_g.restype = i64
+    L.oracle_pbas_frame_g.argtypes = ([i64, i64, vp, i64] + [vp] * 10 + [u64, i32, i32]
+                                      + [f64] * 7 + [i32, vp, i32, vp, vp, f64, f64, vp])
+    L.oracle_pbas_gradient_map.restype = u64
+    L.oracle_pbas_gradient_map.argtypes = [i64, i64, vp, vp]
     L.oracle_pbas_apply_intents.restype = None
     L.oracle_pbas_apply_intents.argtypes = [i64, i32, vp, vp, vp, i64, i32]
     _lib = L
@@ -141,10 +146,15 @@ class OracleEngine:
         self.frame_idx = 0
         self.use_depth = config.mode == "rgbd"
         self.workers = workers if workers is not None else getattr(config, "workers", 1)
+        self.gradient = None
         if config.algorithm == "gmm":
             self.state = gmm_state(width, height, config.gmm)
         else:
             self.state = pbas_state(width, height, config.pbas)
+            self.gradient = getattr(config, "pbas_gradient", None)
+            if self.gradient is not None:  # opt-in feature, see oracle_pbas_frame_g
+                self.state["samples_grad"] = np.zeros((height, width, config.pbas.n), np.uint8)
+                self.state["grad_prev_sum"] = np.full((), GRAD_NONE, dtype=np.uint64)
 
     def state_arrays(self) -> dict:
         return self.state
@@ -166,14 +176,19 @@ class OracleEngine:
             assert rc == 0
         else:
             p = self.config.pbas
-            rc = L.oracle_pbas_frame(
-                self.width, self.height, _p(frame), self.frame_idx,
-                _p(st["samples"]), _p(st["dmin_rgb"]), _p(st["dmin_d"]),
-                _p(st["len_rgb"]), _p(st["pos_rgb"]), _p(st["len_d"]), _p(st["pos_d"]),
-                _p(st["r_rgb"]), _p(st["r_d"]), _p(st["t"]),
-                int(self.config.seed) & _MASK64, p.n, p.min_matches,
-                p.r_lower, p.r_scale, p.r_inc_dec, p.t_lower, p.t_upper, p.t_inc, p.t_dec,
-                int(self.use_depth), _p(mask), self.workers)
+            args = (self.width, self.height, _p(frame), self.frame_idx,
+                    _p(st["samples"]), _p(st["dmin_rgb"]), _p(st["dmin_d"]),
+                    _p(st["len_rgb"]), _p(st["pos_rgb"]), _p(st["len_d"]), _p(st["pos_d"]),
+                    _p(st["r_rgb"]), _p(st["r_d"]), _p(st["t"]),
+                    int(self.config.seed) & _MASK64, p.n, p.min_matches,
+                    p.r_lower, p.r_scale, p.r_inc_dec, p.t_lower, p.t_upper, p.t_inc, p.t_dec,
+                    int(self.use_depth), _p(mask), self.workers)
+            if self.gradient is None:
+                rc = L.oracle_pbas_frame(*args)
+            else:
+                g = self.gradient
+                rc = L.oracle_pbas_frame_g(*args, _p(st["samples_grad"]), _p(st["grad_prev_sum"]),
+                                           float(g.alpha), float(g.mean_init), None)
             assert rc >= 0
         self.frame_idx += 1
         return mask
@@ -206,6 +221,32 @@ def pbas_band_emit(cfg, state, frame, frame_idx, y0, y1, mask):
         p.r_lower, p.r_scale, p.r_inc_dec, p.t_lower, p.t_upper, p.t_inc, p.t_dec,
         int(cfg.mode == "rgbd"), _p(mask), _p(intents), _p(emitters))
     return intents[:k], emitters[:k]
+
+
+GRAD_NONE = (1 << 64) - 1  # grad_prev_sum before the first frame: use mean_init
+
+
+def gradient_map(frame: np.ndarray) -> tuple[np.ndarray, int]:
+    """Opt-in gradient feature's magnitude map (oracle_pbas_gradient_map)."""
+    frame = np.ascontiguousarray(frame, dtype=np.uint8)
+    h, w = frame.shape[:2]
+    g = np.empty((h, w), dtype=np.uint8)
+    total = lib().oracle_pbas_gradient_map(w, h, _p(frame), _p(g))
+    return g, int(total)
+
+
+def gradient_map_np(frame: np.ndarray) -> np.ndarray:
+    """Independent numpy statement of the same map: 3x3 Sobel per channel on
+    an edge-replicated frame, L1 magnitude, max over r,g,b, >> 3."""
+    f = np.pad(frame[:, :, :3].astype(np.int64), ((1, 1), (1, 1), (0, 0)), mode="edge")
+    h, w = frame.shape[:2]
+
+    def at(dy, dx):
+        return f[1 + dy:1 + dy + h, 1 + dx:1 + dx + w]
+
+    sx = (at(-1, 1) + 2 * at(0, 1) + at(1, 1)) - (at(-1, -1) + 2 * at(0, -1) + at(1, -1))
+    sy = (at(1, -1) + 2 * at(1, 0) + at(1, 1)) - (at(-1, -1) + 2 * at(-1, 0) + at(-1, 1))
+    return ((np.abs(sx) + np.abs(sy)).max(axis=2) >> 3).astype(np.uint8)
 
 
 def cpu_threads() -> int:

@@ -175,6 +175,11 @@ typedef struct {
     double r_lower, r_scale, r_inc_dec, t_lower, t_upper, t_inc, t_dec;
     int32_t use_depth;
     uint8_t* mask;
+    /* opt-in gradient feature (NOT in the reference, see oracle_pbas_frame_g);
+     * gsamples == NULL: off */
+    uint8_t* gsamples;   /* (H,W,n) u8 gradient magnitude of every sample */
+    const uint8_t* gmap; /* (H,W) u8 this frame's gradient magnitudes */
+    double cg;           /* alpha / max(previous frame's mean magnitude, 1) */
 } pbas_args;
 
 static const int NBR_DY[8] = {-1, -1, -1, 0, 0, 1, 1, 1}; /* pbas.py:34,340-341 */
@@ -202,22 +207,42 @@ static int64_t pbas_band(const pbas_args* a, int64_t y0, int64_t y1, int64_t* in
                 s[1] = g;
                 s[2] = b;
                 s[3] = d;
+                if (a->gsamples) a->gsamples[pix * n + a->frame_idx] = a->gmap[pix];
                 a->mask[pix] = 0;
                 continue;
             }
 
             int64_t cnt = 0, dminr = 255; /* pbas.py:378-396 */
             double rr = a->r_rgb[pix];
-            for (int64_t i = 0; i < n; ++i) {
-                const uint8_t* s = smp + i * 4;
-                int64_t dr = iabs64((int64_t)r - (int64_t)s[0]);
-                int64_t dg = iabs64((int64_t)g - (int64_t)s[1]);
-                int64_t db = iabs64((int64_t)b - (int64_t)s[2]);
-                int64_t dist = dr;
-                if (dg > dist) dist = dg;
-                if (db > dist) dist = db;
-                if ((double)dist < rr) cnt += 1;
-                if (dist < dminr) dminr = dist;
+            if (!a->gsamples) {
+                for (int64_t i = 0; i < n; ++i) {
+                    const uint8_t* s = smp + i * 4;
+                    int64_t dr = iabs64((int64_t)r - (int64_t)s[0]);
+                    int64_t dg = iabs64((int64_t)g - (int64_t)s[1]);
+                    int64_t db = iabs64((int64_t)b - (int64_t)s[2]);
+                    int64_t dist = dr;
+                    if (dg > dist) dist = dg;
+                    if (db > dist) dist = db;
+                    if ((double)dist < rr) cnt += 1;
+                    if (dist < dminr) dminr = dist;
+                }
+            } else { /* gradient feature: dist + cg * |gm - gm_i|, f64, mul then add */
+                const int64_t gm = a->gmap[pix];
+                const uint8_t* gs = a->gsamples + pix * n;
+                double dminf = 255.0;
+                for (int64_t i = 0; i < n; ++i) {
+                    const uint8_t* s = smp + i * 4;
+                    int64_t dr = iabs64((int64_t)r - (int64_t)s[0]);
+                    int64_t dg = iabs64((int64_t)g - (int64_t)s[1]);
+                    int64_t db = iabs64((int64_t)b - (int64_t)s[2]);
+                    int64_t dist = dr;
+                    if (dg > dist) dist = dg;
+                    if (db > dist) dist = db;
+                    double dd = (double)dist + a->cg * (double)iabs64(gm - (int64_t)gs[i]);
+                    if (dd < rr) cnt += 1;
+                    if (dd < dminf) dminf = dd;
+                }
+                dminr = (int64_t)dminf; /* ring entry: floor, <= 255 */
             }
             int bg_rgb = cnt >= a->min_matches;
 
@@ -294,6 +319,7 @@ static int64_t pbas_band(const pbas_args* a, int64_t y0, int64_t y1, int64_t* in
                     s[1] = g;
                     s[2] = b;
                     s[3] = d;
+                    if (a->gsamples) a->gsamples[pix * n + slot] = a->gmap[pix];
                 }
                 double u1 = oracle_pixel_rng(a->seed, (uint64_t)x, (uint64_t)y,
                                              (uint64_t)a->frame_idx, 1);
@@ -349,6 +375,18 @@ void oracle_pbas_apply_intents(int64_t width, int32_t n, uint8_t* samples, const
     }
 }
 
+/* _apply_intents plus the gradient feature: the target's own magnitude. */
+static void apply_intents_g(int64_t width, int32_t n, uint8_t* samples, const uint8_t* frame,
+                            const int64_t* intents, int64_t count, int32_t use_depth,
+                            uint8_t* gsamples, const uint8_t* gmap) {
+    oracle_pbas_apply_intents(width, n, samples, frame, intents, count, use_depth);
+    if (!gsamples) return;
+    for (int64_t i = 0; i < count; ++i) {
+        int64_t pix = intents[i * 3 + 0] * width + intents[i * 3 + 1];
+        gsamples[pix * n + intents[i * 3 + 2]] = gmap[pix];
+    }
+}
+
 /* Public single-band entry: the reference's PbasState.segment_rows
  * (pbas.py:320-333).  Returns the number of intents written. */
 int64_t oracle_pbas_band(int64_t width, int64_t height, const uint8_t* frame, int64_t frame_idx,
@@ -361,7 +399,7 @@ int64_t oracle_pbas_band(int64_t width, int64_t height, const uint8_t* frame, in
     pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
                    len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
                    seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
-                   t_upper, t_inc, t_dec,   use_depth, mask};
+                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0.0};
     return pbas_band(&a, y0, y1, intents, NULL);
 }
 
@@ -379,7 +417,7 @@ int64_t oracle_pbas_band_emit(int64_t width, int64_t height, const uint8_t* fram
     pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
                    len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
                    seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
-                   t_upper, t_inc, t_dec,   use_depth, mask};
+                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0.0};
     return pbas_band(&a, y0, y1, intents, emitters);
 }
 
@@ -471,18 +509,12 @@ int oracle_gmm_frame(int64_t width, int64_t height, const uint8_t* frame, double
 
 /* One PBAS frame over `workers` row bands, then the sequential intent phase
  * in band order (engine.py:126-143).  Returns total intents applied. */
-int64_t oracle_pbas_frame(int64_t width, int64_t height, const uint8_t* frame, int64_t frame_idx,
-                          uint8_t* samples, uint8_t* dmin_rgb, uint8_t* dmin_d, uint8_t* len_rgb,
-                          uint8_t* pos_rgb, uint8_t* len_d, uint8_t* pos_d, double* r_rgb,
-                          double* r_d, double* t, uint64_t seed, int32_t n, int32_t min_matches,
-                          double r_lower, double r_scale, double r_inc_dec, double t_lower,
-                          double t_upper, double t_inc, double t_dec, int32_t use_depth,
-                          uint8_t* mask, int32_t workers) {
+static int64_t pbas_frame_run(const pbas_args* a, int32_t workers) {
+    const int64_t width = a->width, height = a->height;
+    const int32_t n = a->n, use_depth = a->use_depth;
+    uint8_t* samples = a->samples;
+    const uint8_t* frame = a->frame;
     if (workers < 1) workers = 1;
-    pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
-                   len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
-                   seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
-                   t_upper, t_inc, t_dec,   use_depth, mask};
     int64_t* edges = (int64_t*)malloc(sizeof(int64_t) * (workers + 1));
     band_job* jobs = (band_job*)calloc(workers, sizeof(band_job));
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * workers);
@@ -493,7 +525,7 @@ int64_t oracle_pbas_frame(int64_t width, int64_t height, const uint8_t* frame, i
         j->kind = 1;
         j->y0 = edges[i];
         j->y1 = edges[i + 1];
-        j->pa = &a;
+        j->pa = a;
         int64_t rows = j->y1 - j->y0;
         j->intents = (int64_t*)malloc(sizeof(int64_t) * 3 * (rows * width + 1));
         if (!j->intents) return -1;
@@ -503,8 +535,8 @@ int64_t oracle_pbas_frame(int64_t width, int64_t height, const uint8_t* frame, i
     for (int i = 1; i < workers; ++i) pthread_join(th[i], NULL);
     int64_t total = 0;
     for (int i = 0; i < workers; ++i) {
-        oracle_pbas_apply_intents(width, n, samples, frame, jobs[i].intents, jobs[i].count,
-                                  use_depth);
+        apply_intents_g(width, n, samples, frame, jobs[i].intents, jobs[i].count, use_depth,
+                        a->gsamples, a->gmap);
         total += jobs[i].count;
         free(jobs[i].intents);
     }
@@ -512,4 +544,84 @@ int64_t oracle_pbas_frame(int64_t width, int64_t height, const uint8_t* frame, i
     free(jobs);
     free(th);
     return total;
+}
+
+int64_t oracle_pbas_frame(int64_t width, int64_t height, const uint8_t* frame, int64_t frame_idx,
+                          uint8_t* samples, uint8_t* dmin_rgb, uint8_t* dmin_d, uint8_t* len_rgb,
+                          uint8_t* pos_rgb, uint8_t* len_d, uint8_t* pos_d, double* r_rgb,
+                          double* r_d, double* t, uint64_t seed, int32_t n, int32_t min_matches,
+                          double r_lower, double r_scale, double r_inc_dec, double t_lower,
+                          double t_upper, double t_inc, double t_dec, int32_t use_depth,
+                          uint8_t* mask, int32_t workers) {
+    pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
+                   len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
+                   seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
+                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0.0};
+    return pbas_frame_run(&a, workers);
+}
+
+/* ------------------------------------------- opt-in gradient feature ----
+ * NOT part of the reference (SPEC.md:314 omits the original PBAS gradient
+ * term); this package's definition, restated here as the checker of the
+ * device path (csrc/pbas.cu K2G) -- parity for it is against this
+ * restatement only:
+ *   g(x,y) = max over r,g,b of (|Sx| + |Sy|) >> 3, the 3x3 Sobel responses
+ *            with coordinates clamped into the frame (replicated border);
+ *   sample distance (RGB group) = dist + cg * |g - g_i| in f64 (multiply,
+ *            then add), cg = alpha / max(mean, 1) with mean = the previous
+ *            frame's mean g (mean_init before the first frame);
+ *   dmin ring entry = floor(smallest distance) (<= 255);
+ *   every sample write also stores the magnitude of the pixel observed.
+ * Returns the frame's magnitude sum. */
+uint64_t oracle_pbas_gradient_map(int64_t width, int64_t height, const uint8_t* frame,
+                                  uint8_t* gmap) {
+    uint64_t sum = 0;
+    for (int64_t y = 0; y < height; ++y) {
+        for (int64_t x = 0; x < width; ++x) {
+            int64_t ys[3], xs[3];
+            for (int k = 0; k < 3; ++k) {
+                int64_t yy = y - 1 + k, xx = x - 1 + k;
+                ys[k] = yy < 0 ? 0 : (yy >= height ? height - 1 : yy);
+                xs[k] = xx < 0 ? 0 : (xx >= width ? width - 1 : xx);
+            }
+            int64_t best = 0;
+            for (int c = 0; c < 3; ++c) {
+#define PX(i, j) ((int64_t)frame[(ys[i] * width + xs[j]) * 4 + c])
+                int64_t sx = (PX(0, 2) + 2 * PX(1, 2) + PX(2, 2)) - (PX(0, 0) + 2 * PX(1, 0) + PX(2, 0));
+                int64_t sy = (PX(2, 0) + 2 * PX(2, 1) + PX(2, 2)) - (PX(0, 0) + 2 * PX(0, 1) + PX(0, 2));
+#undef PX
+                int64_t m = iabs64(sx) + iabs64(sy);
+                if (m > best) best = m;
+            }
+            gmap[y * width + x] = (uint8_t)(best >> 3);
+            sum += (uint64_t)(best >> 3);
+        }
+    }
+    return sum;
+}
+
+/* One PBAS frame with the gradient feature.  *prev_sum: the previous frame's
+ * magnitude sum (UINT64_MAX before the first frame); updated to this
+ * frame's.  gmap_out (H*W u8, may be NULL) receives the magnitude map. */
+int64_t oracle_pbas_frame_g(int64_t width, int64_t height, const uint8_t* frame, int64_t frame_idx,
+                            uint8_t* samples, uint8_t* dmin_rgb, uint8_t* dmin_d, uint8_t* len_rgb,
+                            uint8_t* pos_rgb, uint8_t* len_d, uint8_t* pos_d, double* r_rgb,
+                            double* r_d, double* t, uint64_t seed, int32_t n, int32_t min_matches,
+                            double r_lower, double r_scale, double r_inc_dec, double t_lower,
+                            double t_upper, double t_inc, double t_dec, int32_t use_depth,
+                            uint8_t* mask, int32_t workers, uint8_t* gsamples, uint64_t* prev_sum,
+                            double alpha, double mean_init, uint8_t* gmap_out) {
+    uint8_t* gmap = gmap_out ? gmap_out : (uint8_t*)malloc((size_t)(width * height));
+    if (!gmap) return -1;
+    const uint64_t sum = oracle_pbas_gradient_map(width, height, frame, gmap);
+    double mean = *prev_sum == UINT64_MAX ? mean_init : (double)*prev_sum / (double)(width * height);
+    pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
+                   len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
+                   seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
+                   t_upper, t_inc, t_dec,   use_depth, mask, gsamples, gmap,
+                   alpha / (mean > 1.0 ? mean : 1.0)};
+    int64_t rc = pbas_frame_run(&a, workers);
+    *prev_sum = sum;
+    if (!gmap_out) free(gmap);
+    return rc;
 }

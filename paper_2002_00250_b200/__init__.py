@@ -7,7 +7,7 @@ kernels (csrc/) behind a C-ABI (include/rgbdseg_b200.h); there is no CPU
 fallback — a missing extension raises `DeviceError`.
 """
 
-from .config import GmmParams, PbasParams, PipelineConfig
+from .config import GmmParams, PbasGradient, PbasParams, PipelineConfig
 from .errors import (
     ConfigError,
     DeviceError,
@@ -40,7 +40,7 @@ def __getattr__(name):
 
 
 __all__ = [
-    "GmmParams", "PbasParams", "PipelineConfig", "SegmentationEngine", "MultiStreamEngine",
+    "GmmParams", "PbasGradient", "PbasParams", "PipelineConfig", "SegmentationEngine", "MultiStreamEngine",
     "pixel_rng", "rng_stream", "process_sequence", "RunStats", "MemorySequence", "RgbdSegError",
     "DimensionError", "FormatError",
     "SequenceError", "ConfigError", "DeviceError", "__version__",

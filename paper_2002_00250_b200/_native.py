@@ -37,14 +37,16 @@ EXPORTS = (
     "rgbdseg_halo_link_set_timeout", "rgbdseg_halo_link_status", "rgbdseg_halo_link_destroy",
     "rgbdseg_selftest_fdiv", "rgbdseg_gmm_set_eval", "rgbdseg_gmm_eval_counts",
     "rgbdseg_pbas_set_eval", "rgbdseg_pbas_eval_counts", "rgbdseg_pbas_set_k2_mode",
-    "rgbdseg_pbas_get_k2_mode",
+    "rgbdseg_pbas_get_k2_mode", "rgbdseg_pbas_set_gradient",
 )
 
 IPC_HANDLE_BYTES = 64  # RGBDSEG_IPC_HANDLE_BYTES
 
 GMM_FIELDS = {"rgb_w": 0, "rgb_mu": 1, "rgb_var": 2, "d_w": 3, "d_mu": 4, "d_var": 5}
 PBAS_FIELDS = {"samples": 0, "dmin_rgb": 1, "dmin_d": 2, "len_rgb": 3, "pos_rgb": 4,
-               "len_d": 5, "pos_d": 6, "r_rgb": 7, "r_d": 8, "t": 9}
+               "len_d": 5, "pos_d": 6, "r_rgb": 7, "r_d": 8, "t": 9,
+               # opt-in gradient feature (config.PbasGradient) only
+               "samples_grad": 10, "grad_prev_sum": 11}
 
 
 class GmmParamsC(ctypes.Structure):
@@ -125,6 +127,7 @@ def _declare(L):
         "rgbdseg_pbas_eval_counts": (ctypes.c_int, [vp, vp, i32, i32, vp]),
         "rgbdseg_pbas_set_k2_mode": (ctypes.c_int, [vp, i32]),
         "rgbdseg_pbas_get_k2_mode": (i32, [vp]),
+        "rgbdseg_pbas_set_gradient": (ctypes.c_int, [vp, i32, ctypes.c_double, ctypes.c_double]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

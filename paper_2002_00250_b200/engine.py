@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _native
 from .config import validate_config
-from .errors import DeviceError, DimensionError
+from .errors import ConfigError, DeviceError, DimensionError
 
 _GMM_SHAPES = {
     "rgb_w": lambda h, w, p: ((h, w, p.k_rgb), np.float64),
@@ -49,6 +49,11 @@ _PBAS_SHAPES = {
     "r_rgb": lambda h, w, p: ((h, w), np.float64),
     "r_d": lambda h, w, p: ((h, w), np.float64),
     "t": lambda h, w, p: ((h, w), np.float64),
+}
+# opt-in gradient feature (config.PbasGradient; not in the reference)
+_PBAS_GRAD_SHAPES = {
+    "samples_grad": lambda h, w, p: ((h, w, p.n), np.uint8),
+    "grad_prev_sum": lambda h, w, p: ((), np.uint64),
 }
 
 
@@ -131,7 +136,7 @@ class StateView(Mapping):
         self._eng = engine
 
     def _shapes(self):
-        return _GMM_SHAPES if self._eng.config.algorithm == "gmm" else _PBAS_SHAPES
+        return self._eng._shapes()
 
     def __getitem__(self, key):
         shapes = self._shapes()
@@ -166,6 +171,14 @@ class SegmentationEngine:
         self._h = _Handle(config.algorithm, self.width, self.height, params, self.use_depth,
                           config.seed, self.device, band=_band)
         self._gmm_frame_idx = 0
+        self.gradient = getattr(config, "pbas_gradient", None) if config.algorithm == "pbas" else None
+        if self.gradient is not None:  # opt-in extension, K2G (csrc/pbas.cu)
+            if _band is not None:
+                self.close()
+                raise ConfigError("the PBAS gradient feature needs the whole frame (no row bands)")
+            rc = self._h.fn("set_gradient")(self._h.ptr, 1, float(self.gradient.alpha),
+                                            float(self.gradient.mean_init))
+            _native.check(rc, "set_gradient")
 
     # ----------------------------------------------------------- surface --
     @property
@@ -337,8 +350,15 @@ class SegmentationEngine:
         self._gmm_frame_idx += 1
 
     # ------------------------------------------------------------- state --
+    def _shapes(self):
+        if self.config.algorithm == "gmm":
+            return _GMM_SHAPES
+        return {**_PBAS_SHAPES, **_PBAS_GRAD_SHAPES} if self.gradient is not None else _PBAS_SHAPES
+
     def _field_spec(self, key):
-        shapes = _GMM_SHAPES if self.config.algorithm == "gmm" else _PBAS_SHAPES
+        shapes = self._shapes()
+        if key not in shapes:
+            raise KeyError(key)
         fields = _native.GMM_FIELDS if self.config.algorithm == "gmm" else _native.PBAS_FIELDS
         shape, dtype = shapes[key](self.rows, self.width, self._params)
         return fields[key], shape, dtype
@@ -357,7 +377,7 @@ class SegmentationEngine:
         self._sync_external()
         for key, value in arrays.items():
             fid, shape, dtype = self._field_spec(key)
-            arr = np.ascontiguousarray(value, dtype=dtype)
+            arr = np.asarray(value, dtype=dtype, order="C")  # keeps 0-d fields 0-d
             if arr.shape != shape:
                 raise DimensionError(f"state field {key}: expected {shape}, got {arr.shape}")
             rc = self._h.fn("write_state")(self._h.ptr, fid, arr.ctypes.data, arr.nbytes)
