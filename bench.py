@@ -56,12 +56,15 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 from paper_2002_00250_b200 import synth  # noqa: E402
-from paper_2002_00250_b200.config import GmmParams, PbasParams, PipelineConfig  # noqa: E402
+from paper_2002_00250_b200.config import (GmmParams, PbasGradient, PbasParams,  # noqa: E402
+                                          PipelineConfig)
 
 METRIC = "Mpixel/s and fps at 1920x1080 RGB-D (GMM, PBAS), 1/2/4/8 B200, % HBM roofline"
 UNIT = "Mpixel/s"
 # SURVEY.md §8(d) algorithmic bytes per pixel per frame (B_alg).
-B_ALG = {("gmm", 7, 3): 485, ("gmm", 3, 3): 293, ("pbas", 20): 181}
+B_ALG = {("gmm", 7, 3): 485, ("gmm", 3, 3): 293, ("pbas", 20): 181,
+         # opt-in gradient feature (--pbas-gradient): + n bytes of per-sample magnitudes read
+         ("pbas_grad", 20): 201}
 
 WORKLOADS = {
     # name: (width, height, streams per GPU, gmm (k_rgb, k_d) or None, pbas n or None)
@@ -274,10 +277,12 @@ def run_ours(args, rank, world, local_rank):
         ring_s = torch.from_numpy(_gen_ring("S", w, h, stream_ids, gmm_k[0], gmm_k[0])).to(dev)
         algos.append(("gmm", g, ring_s, B_ALG.get(("gmm",) + tuple(gmm_k))))
     if pbas_n:
-        pcfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=pbas_n))
+        pcfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=pbas_n),
+                              pbas_gradient=PbasGradient() if args.pbas_gradient else None)
         p = MultiStreamEngine(pcfg, w, h, S, device=local_rank, seeds=[s + 1 for s in stream_ids])
         ring_t = torch.from_numpy(_gen_ring("T", w, h, stream_ids, 8)).to(dev)
-        algos.append(("pbas", p, ring_t, B_ALG.get(("pbas", pbas_n))))
+        algos.append(("pbas", p, ring_t,
+                      B_ALG.get(("pbas_grad" if args.pbas_gradient else "pbas", pbas_n))))
     # One CUDA stream and one mask buffer per algorithm: GMM (HBM-bound) and
     # PBAS (latency-bound K3) are independent engines and run concurrently.
     # PBAS (latency-bound) on a higher-priority stream: the block scheduler
@@ -465,7 +470,9 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         wl_desc = (f"{args.workload}: {S} x {w}x{h} RGB-D streams per GPU"
                    + (f", GMM {gmm_k[0]}/{gmm_k[1]} (regime S)" if gmm_k else "")
-                   + (f", PBAS n={pbas_n} (regime T)" if pbas_n else ""))
+                   + (f", PBAS n={pbas_n} (regime T)" if pbas_n else "")
+                   + (" with the opt-in gradient feature (not the reference algorithm)"
+                      if pbas_n and args.pbas_gradient else ""))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -474,6 +481,9 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": wl_desc, "width": w, "height": h, "streams_per_gpu": S,
                        "streams_total": S * world,
                        "gmm": list(gmm_k) if gmm_k else None, "pbas_n": pbas_n,
+                       "pbas_gradient": ({"alpha": PbasGradient().alpha,
+                                          "mean_init": PbasGradient().mean_init}
+                                         if args.pbas_gradient else None),
                        "burn_in_frames": burn,
                        "l2": (f"inputs larger than L2 (state per step {state_bytes / 1e9:.2f} GB "
                               f">> {l2_bytes >> 20} MB)" if flush_buf is None else
@@ -639,6 +649,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
     ap.add_argument("--streams", type=int, default=0, help="override streams per GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pbas-gradient", action="store_true",
+                    help="PBAS with the opt-in gradient feature (K2G; not the reference algorithm)")
     ap.add_argument("--stream-priority", type=int, default=0,
                     help="PBAS stream priority boost over GMM (0 = equal)")
     ap.add_argument("--e2e-steps", type=int, default=50)

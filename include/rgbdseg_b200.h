@@ -222,8 +222,9 @@ void rgbdseg_halo_link_destroy(rgbdseg_halo_link* l);
  * reference drops the original PBAS gradient term; semantics in
  * DESIGN.md §3 "K2G", CPU checker oracle_pbas_frame_g).  Switched before the
  * first frame of a single-band handle: enable = 1 with alpha >= 0 (sample
- * distance dist + alpha / max(mean g of the previous frame, 1) * |g - g_i|)
- * and mean_init > 0 (the mean before the first frame); enable = 0 returns to
+ * distance 256 dist + w |g - g_i| against 256 R, w = min(65535, floor(alpha *
+ * 256 / max(mean g of the previous frame, 1) + 0.5))) and mean_init > 0 (the
+ * mean before the first frame); enable = 0 returns to
  * the reference algorithm.  Adds state fields RGBDSEG_PBAS_GSAMPLES and
  * RGBDSEG_PBAS_GRAD_PREV. */
 int rgbdseg_pbas_set_gradient(rgbdseg_pbas* h, int32_t enable, double alpha, double mean_init);

@@ -61,6 +61,8 @@ def lib():
     L.oracle_pbas_frame_g.restype = i64
     L.oracle_pbas_frame_g.argtypes = ([i64, i64, vp, i64] + [vp] * 10 + [u64, i32, i32]
                                       + [f64] * 7 + [i32, vp, i32, vp, vp, f64, f64, vp])
+    L.oracle_pbas_gradient_weight.restype = ctypes.c_uint32
+    L.oracle_pbas_gradient_weight.argtypes = [u64, i64, f64, f64]
     L.oracle_pbas_gradient_map.restype = u64
     L.oracle_pbas_gradient_map.argtypes = [i64, i64, vp, vp]
     L.oracle_pbas_apply_intents.restype = None
@@ -233,6 +235,10 @@ def gradient_map(frame: np.ndarray) -> tuple[np.ndarray, int]:
     g = np.empty((h, w), dtype=np.uint8)
     total = lib().oracle_pbas_gradient_map(w, h, _p(frame), _p(g))
     return g, int(total)
+
+
+def gradient_weight(prev_sum: int, npix: int, alpha: float, mean_init: float) -> int:
+    return int(lib().oracle_pbas_gradient_weight(prev_sum, npix, alpha, mean_init))
 
 
 def gradient_map_np(frame: np.ndarray) -> np.ndarray:

@@ -179,7 +179,7 @@ typedef struct {
      * gsamples == NULL: off */
     uint8_t* gsamples;   /* (H,W,n) u8 gradient magnitude of every sample */
     const uint8_t* gmap; /* (H,W) u8 this frame's gradient magnitudes */
-    double cg;           /* alpha / max(previous frame's mean magnitude, 1) */
+    int64_t gw;          /* the frame's gradient weight in 1/256 units */
 } pbas_args;
 
 static const int NBR_DY[8] = {-1, -1, -1, 0, 0, 1, 1, 1}; /* pbas.py:34,340-341 */
@@ -226,10 +226,10 @@ static int64_t pbas_band(const pbas_args* a, int64_t y0, int64_t y1, int64_t* in
                     if ((double)dist < rr) cnt += 1;
                     if (dist < dminr) dminr = dist;
                 }
-            } else { /* gradient feature: dist + cg * |gm - gm_i|, f64, mul then add */
+            } else { /* gradient feature: 256 dist + gw |gm - gm_i| against 256 R */
                 const int64_t gm = a->gmap[pix];
                 const uint8_t* gs = a->gsamples + pix * n;
-                double dminf = 255.0;
+                int64_t dmin256 = 255 * 256;
                 for (int64_t i = 0; i < n; ++i) {
                     const uint8_t* s = smp + i * 4;
                     int64_t dr = iabs64((int64_t)r - (int64_t)s[0]);
@@ -238,11 +238,11 @@ static int64_t pbas_band(const pbas_args* a, int64_t y0, int64_t y1, int64_t* in
                     int64_t dist = dr;
                     if (dg > dist) dist = dg;
                     if (db > dist) dist = db;
-                    double dd = (double)dist + a->cg * (double)iabs64(gm - (int64_t)gs[i]);
-                    if (dd < rr) cnt += 1;
-                    if (dd < dminf) dminf = dd;
+                    int64_t dd = 256 * dist + a->gw * iabs64(gm - (int64_t)gs[i]);
+                    if ((double)dd < 256.0 * rr) cnt += 1; /* both sides exact */
+                    if (dd < dmin256) dmin256 = dd;
                 }
-                dminr = (int64_t)dminf; /* ring entry: floor, <= 255 */
+                dminr = dmin256 >> 8; /* ring entry: floor(min / 256) <= 255 */
             }
             int bg_rgb = cnt >= a->min_matches;
 
@@ -399,7 +399,7 @@ int64_t oracle_pbas_band(int64_t width, int64_t height, const uint8_t* frame, in
     pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
                    len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
                    seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
-                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0.0};
+                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0};
     return pbas_band(&a, y0, y1, intents, NULL);
 }
 
@@ -417,7 +417,7 @@ int64_t oracle_pbas_band_emit(int64_t width, int64_t height, const uint8_t* fram
     pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
                    len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
                    seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
-                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0.0};
+                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0};
     return pbas_band(&a, y0, y1, intents, emitters);
 }
 
@@ -556,7 +556,7 @@ int64_t oracle_pbas_frame(int64_t width, int64_t height, const uint8_t* frame, i
     pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
                    len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
                    seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
-                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0.0};
+                   t_upper, t_inc, t_dec,   use_depth, mask, NULL, NULL, 0};
     return pbas_frame_run(&a, workers);
 }
 
@@ -567,10 +567,13 @@ int64_t oracle_pbas_frame(int64_t width, int64_t height, const uint8_t* frame, i
  * restatement only:
  *   g(x,y) = max over r,g,b of (|Sx| + |Sy|) >> 3, the 3x3 Sobel responses
  *            with coordinates clamped into the frame (replicated border);
- *   sample distance (RGB group) = dist + cg * |g - g_i| in f64 (multiply,
- *            then add), cg = alpha / max(mean, 1) with mean = the previous
- *            frame's mean g (mean_init before the first frame);
- *   dmin ring entry = floor(smallest distance) (<= 255);
+ *   sample distance (RGB group), in 1/256 units:
+ *            D_i = 256 dist_i + w |g - g_i|, a match when D_i < 256 R
+ *            (exact: D_i < 2^24 and 256 R are both exact doubles), with the
+ *            frame's integer weight w = min(65535, floor(alpha * 256 / m +
+ *            0.5)), m = max(mean, 1), mean = the previous frame's mean g
+ *            (prev_sum / (W H), f64) or mean_init before the first frame;
+ *   dmin ring entry = floor(min_i D_i / 256), capped at 255;
  *   every sample write also stores the magnitude of the pixel observed.
  * Returns the frame's magnitude sum. */
 uint64_t oracle_pbas_gradient_map(int64_t width, int64_t height, const uint8_t* frame,
@@ -600,6 +603,14 @@ uint64_t oracle_pbas_gradient_map(int64_t width, int64_t height, const uint8_t* 
     return sum;
 }
 
+/* The frame's weight w from the previous frame's magnitude sum. */
+uint32_t oracle_pbas_gradient_weight(uint64_t prev_sum, int64_t npix, double alpha,
+                                     double mean_init) {
+    const double mean = prev_sum == UINT64_MAX ? mean_init : (double)prev_sum / (double)npix;
+    const double q = floor(alpha * 256.0 / (mean > 1.0 ? mean : 1.0) + 0.5);
+    return q > 65535.0 ? 65535u : (uint32_t)q;
+}
+
 /* One PBAS frame with the gradient feature.  *prev_sum: the previous frame's
  * magnitude sum (UINT64_MAX before the first frame); updated to this
  * frame's.  gmap_out (H*W u8, may be NULL) receives the magnitude map. */
@@ -614,12 +625,12 @@ int64_t oracle_pbas_frame_g(int64_t width, int64_t height, const uint8_t* frame,
     uint8_t* gmap = gmap_out ? gmap_out : (uint8_t*)malloc((size_t)(width * height));
     if (!gmap) return -1;
     const uint64_t sum = oracle_pbas_gradient_map(width, height, frame, gmap);
-    double mean = *prev_sum == UINT64_MAX ? mean_init : (double)*prev_sum / (double)(width * height);
     pbas_args a = {width, height,  frame,   frame_idx, samples, dmin_rgb,  dmin_d,
                    len_rgb, pos_rgb, len_d, pos_d,   r_rgb,   r_d,       t,
                    seed,  n,       min_matches, r_lower, r_scale, r_inc_dec, t_lower,
                    t_upper, t_inc, t_dec,   use_depth, mask, gsamples, gmap,
-                   alpha / (mean > 1.0 ? mean : 1.0)};
+                   (int64_t)oracle_pbas_gradient_weight(*prev_sum, width * height, alpha,
+                                                        mean_init)};
     int64_t rc = pbas_frame_run(&a, workers);
     *prev_sum = sum;
     if (!gmap_out) free(gmap);

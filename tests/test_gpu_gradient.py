@@ -45,6 +45,9 @@ def _compare_run(oracle_mod, cfg, w, h, frames, workers=2):
 @pytest.mark.parametrize("w,h,n,mm,mode,alpha", [
     (45, 31, 6, 2, "rgbd", 10.0),      # ragged in x and y
     (64, 16, 20, 2, "rgbd", 10.0),     # the paper's n, whole tiles
+    (45, 13, 20, 1, "rgbd", 10.0),     # n = 20 order statistics, min_matches 1
+    (40, 12, 20, 3, "rgbd", 10.0),     # n = 20 with counters
+    (64, 16, 20, 2, "rgb_only", 60.0), # large weight
     (33, 9, 40, 2, "rgbd", 4.0),       # u16 intent codes
     (50, 23, 7, 1, "rgb_only", 10.0),
     (37, 19, 9, 3, "rgbd", 25.0),

@@ -94,7 +94,7 @@ def _py_frame(oracle_mod, st, frame, f, cfg, prev_sum):
     use_depth = cfg.mode == "rgbd"
     gmap = oracle_mod.gradient_map_np(frame).astype(int)
     mean = g.mean_init if prev_sum is None else prev_sum / (h * w)
-    cg = g.alpha / (mean if mean > 1.0 else 1.0)
+    wt = min(65535, int(math.floor(g.alpha * 256.0 / (mean if mean > 1.0 else 1.0) + 0.5)))
     mask = np.zeros((h, w), np.uint8)
     intents = []
     S, G = st["samples"], st["samples_grad"]
@@ -107,14 +107,14 @@ def _py_frame(oracle_mod, st, frame, f, cfg, prev_sum):
                 S[y, x, f] = (r, gg, b, d)
                 G[y, x, f] = gm
                 continue
-            cnt, dminf = 0, 255.0
+            cnt, dmin256 = 0, 255 * 256
             for i in range(n):
                 sr, sg, sb, _ = (int(v) for v in S[y, x, i])
                 dist = max(abs(r - sr), abs(gg - sg), abs(b - sb))
-                dd = float(dist) + cg * float(abs(gm - int(G[y, x, i])))
-                cnt += dd < st["r_rgb"][y, x]
-                dminf = min(dminf, dd)
-            dminr = int(math.floor(dminf))
+                dd = 256 * dist + wt * abs(gm - int(G[y, x, i]))
+                cnt += dd < 256 * st["r_rgb"][y, x]  # exact: int vs a power-of-two multiple
+                dmin256 = min(dmin256, dd)
+            dminr = dmin256 >> 8
             bg_rgb = cnt >= p.min_matches
             depth_eval, bg_depth, dmind = False, True, 255
             if d > 0:
@@ -169,6 +169,16 @@ def _py_frame(oracle_mod, st, frame, f, cfg, prev_sum):
         S[ny, nx, slot] = (*frame[ny, nx, :3], frame[ny, nx, 3] if use_depth else 0)
         G[ny, nx, slot] = gmap[ny, nx]
     return mask, int(gmap.sum())
+
+
+def test_gradient_weight(oracle_mod):
+    none = oracle_mod.GRAD_NONE
+    assert oracle_mod.gradient_weight(none, 100, 10.0, 20.0) == 128  # 2560 / 20
+    assert oracle_mod.gradient_weight(2000, 100, 10.0, 20.0) == 128  # mean 20
+    assert oracle_mod.gradient_weight(0, 100, 10.0, 20.0) == 2560    # mean floored at 1
+    assert oracle_mod.gradient_weight(0, 100, 1e9, 20.0) == 65535    # capped
+    assert oracle_mod.gradient_weight(0, 100, 0.0, 20.0) == 0
+    assert oracle_mod.gradient_weight(300, 100, 1.0, 20.0) == 85     # 256/3 = 85.33
 
 
 @pytest.mark.parametrize("mode,alpha,seed", [("rgbd", 10.0, 11), ("rgb_only", 3.5, 12)])
