@@ -64,7 +64,9 @@ UNIT = "Mpixel/s"
 # SURVEY.md §8(d) algorithmic bytes per pixel per frame (B_alg).
 B_ALG = {("gmm", 7, 3): 485, ("gmm", 3, 3): 293, ("pbas", 20): 181,
          # opt-in gradient feature (--pbas-gradient): + n bytes of per-sample magnitudes read
-         ("pbas_grad", 20): 201}
+         ("pbas_grad", 20): 201,
+         # opt-in f32 GMM state storage (--gmm-state f32)
+         ("gmm_f32", 7, 3): 245, ("gmm_f32", 3, 3): 149}
 
 WORKLOADS = {
     # name: (width, height, streams per GPU, gmm (k_rgb, k_d) or None, pbas n or None)
@@ -87,18 +89,62 @@ def measured_peaks():
 
 # ----------------------------------------------------------------- clocks --
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 50 ms."""
+    """SM clocks + throttle reasons sampled every 2 ms through NVML (a polling
+    thread, so even a ~0.2 s warm-up + timed region gets ~100 samples);
+    falls back to `nvidia-smi -lms 50` when NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, pci_bus_id: str | None = None):
         self.gpu = gpu_index
+        self.pci = pci_bus_id
         self.proc = None
         self.f = None
+        self.thread = None
+        self.samples = []
+
+    def _nvml_start(self) -> bool:
+        try:
+            import threading
+
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = None
+            if self.pci and "RGBDSEG_NVSMI_INDEX" not in os.environ:
+                try:
+                    h = nv.nvmlDeviceGetHandleByPciBusId(self.pci)
+                except Exception:
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        except Exception:
+            return False
+        self._stop = threading.Event()
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((mhz, max_mhz, {n for n, b in zip(self.NAMES, bits) if r & b}))
+                except Exception:
+                    pass
+                self._stop.wait(0.002)
+
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
+        return True
 
     def start(self):
+        if self._nvml_start():
+            return
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
@@ -109,31 +155,55 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.f.flush()
-        rows = [ln.split(",") for ln in Path(self.f.name).read_text().splitlines() if ln.strip()]
-        os.unlink(self.f.name)
-        sms, maxes, reasons = [], [], set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for r in rows:
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=5)
+            rows = self.samples
+            src = "nvml"
+        elif self.proc is not None:
+            self.proc.terminate()
             try:
-                sms.append(float(r[1]))
-                maxes.append(float(r[2]))
-            except (ValueError, IndexError):
-                continue
-            for nm, v in zip(names, r[4:8]):
-                if v.strip().lower() == "active":
-                    reasons.add(nm)
-        if not sms:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.flush()
+            rows = []
+            for ln in Path(self.f.name).read_text().splitlines():
+                r = ln.split(",")
+                try:
+                    rows.append((float(r[1]), float(r[2]),
+                                 {n for n, v in zip(self.NAMES, r[4:8]) if v.strip().lower() == "active"}))
+                except (ValueError, IndexError):
+                    continue
+            os.unlink(self.f.name)
+            src = "nvidia-smi"
+        else:
             return None
-        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(maxes),
-                "reasons": sorted(reasons), "samples": len(sms)}
+        if not rows:
+            return None
+        reasons = set().union(*(r[2] for r in rows))
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows), "source": src}
+
+
+def _throttled(clock_info, dev, world) -> bool:
+    """hw_slowdown / hw_thermal_slowdown / sw_thermal_slowdown seen on any rank
+    (sw_power_cap is kept and noted)."""
+    bad = bool(clock_info and set(clock_info["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown",
+                                                            "sw_thermal_slowdown"})
+    if world > 1:
+        flag = torch.tensor([int(bad)], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        bad = bool(flag.item())
+    return bad
+
+
+def _pci_bus_id(dev) -> str | None:
+    try:
+        p = torch.cuda.get_device_properties(dev)
+        return f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    except Exception:
+        return None
 
 
 # --------------------------------------------------------------- frames ---
@@ -272,10 +342,12 @@ def run_ours(args, rank, world, local_rank):
     # ---- engines + device frame rings (untimed setup)
     algos = []
     if gmm_k:
-        gcfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=gmm_k[0], k_d=gmm_k[1]))
+        gcfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=gmm_k[0], k_d=gmm_k[1]),
+                              gmm_state_dtype="float32" if args.gmm_state == "f32" else "float64")
         g = MultiStreamEngine(gcfg, w, h, S, device=local_rank, seeds=[s + 1 for s in stream_ids])
         ring_s = torch.from_numpy(_gen_ring("S", w, h, stream_ids, gmm_k[0], gmm_k[0])).to(dev)
-        algos.append(("gmm", g, ring_s, B_ALG.get(("gmm",) + tuple(gmm_k))))
+        algos.append(("gmm", g, ring_s,
+                      B_ALG.get(("gmm_f32" if args.gmm_state == "f32" else "gmm",) + tuple(gmm_k))))
     if pbas_n:
         pcfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=pbas_n),
                               pbas_gradient=PbasGradient() if args.pbas_gradient else None)
@@ -310,8 +382,15 @@ def run_ours(args, rank, world, local_rank):
                  if state_bytes < 4 * l2_bytes else None)
 
     def flush_l2(k):
+        # 2x-L2 write (evicts every line of the workload), then -- unless
+        # --flush write -- a read pass over the same buffer so the dirty
+        # flush lines are written back HERE, untimed, and the timed step
+        # starts from a cold but clean L2 (otherwise the step pays the
+        # flush's own ~126 MB write-back).
         if flush_buf is not None:
             flush_buf.fill_(k & 0xFF)
+            if args.flush == "write+read":
+                flush_buf.amax()
 
     burn = max([8 if a[0] == "gmm" else 2 * pbas_n for a in algos])
     for t in range(burn):
@@ -358,40 +437,46 @@ def run_ours(args, rank, world, local_rank):
             launch(name, eng, ring, t_frame_by[name])
             t_frame_by[name] += 1
 
-    clocks = ClockSampler(int(os.environ.get("RGBDSEG_NVSMI_INDEX", local_rank)))
-    clocks.start()  # sampling spans warm-up + timed region (both under full load)
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    def timed(n):
-        """n steps between one event pair (fork/join of the algorithm streams)."""
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        start.record(main)
-        for name in streams:
-            if streams[name] is not main:
-                streams[name].wait_event(start)
-        for _ in range(n):
+    remeasured = False
+    for attempt in range(2):  # a throttled run (hw/thermal slowdown) is re-measured once
+        clocks = ClockSampler(int(os.environ.get("RGBDSEG_NVSMI_INDEX", local_rank)), _pci_bus_id(dev))
+        clocks.start()  # sampling spans warm-up + timed region (both under full load)
+        for _ in range(args.warmup):
             step()
-        for name in streams:
-            if streams[name] is not main:
-                done = torch.cuda.Event()
-                done.record(streams[name])
-                main.wait_event(done)
-        end.record(main)
-        return start, end
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        def timed(n):
+            """n steps between one event pair (fork/join of the algorithm streams)."""
+            start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record(main)
+            for name in streams:
+                if streams[name] is not main:
+                    streams[name].wait_event(start)
+            for _ in range(n):
+                step()
+            for name in streams:
+                if streams[name] is not main:
+                    done = torch.cuda.Event()
+                    done.record(streams[name])
+                    main.wait_event(done)
+            end.record(main)
+            return start, end
 
-    if flush_buf is None:
-        spans = [timed(args.steps)]
-    else:  # cold L2 every step: flush on main (untimed), then one timed step
-        spans = []
-        for k in range(args.steps):
-            flush_l2(k)
-            spans.append(timed(1))
-    torch.cuda.synchronize()
-    clock_info = clocks.stop()
+        if flush_buf is None:
+            spans = [timed(args.steps)]
+        else:  # cold L2 every step: flush on main (untimed), then one timed step
+            spans = []
+            for k in range(args.steps):
+                flush_l2(k)
+                spans.append(timed(1))
+        torch.cuda.synchronize()
+        clock_info = clocks.stop()
+        if attempt == 0 and _throttled(clock_info, dev, world):
+            remeasured = True
+            continue
+        break
     if world > 1:
         dist.barrier()
     elapsed_ms = sum(a.elapsed_time(b) for a, b in spans)
@@ -472,22 +557,26 @@ def run_ours(args, rank, world, local_rank):
                    + (f", GMM {gmm_k[0]}/{gmm_k[1]} (regime S)" if gmm_k else "")
                    + (f", PBAS n={pbas_n} (regime T)" if pbas_n else "")
                    + (" with the opt-in gradient feature (not the reference algorithm)"
-                      if pbas_n and args.pbas_gradient else ""))
+                      if pbas_n and args.pbas_gradient else "")
+                   + (" with opt-in f32 GMM state storage (north_star tolerance, not bit parity)"
+                      if gmm_k and args.gmm_state == "f32" else ""))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64/u8",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 (f32 GMM state)/u8" if gmm_k and args.gmm_state == "f32" else "f64/u8",
             "data": "synthetic (SURVEY.md §8(d) regimes S/T, seeded per stream)",
             "config": {"workload": wl_desc, "width": w, "height": h, "streams_per_gpu": S,
                        "streams_total": S * world,
                        "gmm": list(gmm_k) if gmm_k else None, "pbas_n": pbas_n,
+                       "gmm_state": args.gmm_state if gmm_k else None,
                        "pbas_gradient": ({"alpha": PbasGradient().alpha,
                                           "mean_init": PbasGradient().mean_init}
                                          if args.pbas_gradient else None),
                        "burn_in_frames": burn,
                        "l2": (f"inputs larger than L2 (state per step {state_bytes / 1e9:.2f} GB "
                               f">> {l2_bytes >> 20} MB)" if flush_buf is None else
-                              f"L2 flushed between timed steps ({2 * l2_bytes >> 20} MB write, "
+                              f"L2 flushed between timed steps ({2 * l2_bytes >> 20} MB {args.flush}, "
                               f"untimed; state per step {state_bytes / 1e6:.0f} MB < 4x L2), "
                               "each step timed by its own event pair"),
                        "parallelism": f"streams sharded {S}/GPU over {world} GPU(s)",
@@ -500,7 +589,7 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
-            "clocks": clock_info,
+            "clocks": (dict(clock_info, remeasured=remeasured) if clock_info else None),
             "fg_fraction_last_step": float(counters[0].item()) / float(counters[1].item()),
             "model_age": age_info,
         }
@@ -534,7 +623,7 @@ def run_config5(args, rank, world, local_rank):
     for _ in range(2 * n):  # burn-in: warm-up fill + full dmin rings
         band.step(ring[t % 4], mask)
         t += 1
-    clocks = ClockSampler(int(os.environ.get("RGBDSEG_NVSMI_INDEX", local_rank)))
+    clocks = ClockSampler(int(os.environ.get("RGBDSEG_NVSMI_INDEX", local_rank)), _pci_bus_id(dev))
     clocks.start()  # sampling spans warm-up + timed region (both under full load)
     for _ in range(args.warmup):  # BASELINE config 5 is a 60-frame sequence: stay young
         band.step(ring[t % 4], mask)
@@ -649,6 +738,11 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
     ap.add_argument("--streams", type=int, default=0, help="override streams per GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gmm-state", choices=["f64", "f32"], default="f64",
+                    help="GMM state storage: f64 = the reference's (default, bit parity); "
+                         "f32 = opt-in half-width storage (north_star tolerance)")
+    ap.add_argument("--flush", choices=["write+read", "write"], default="write+read",
+                    help="L2 flush between timed steps of the small configs (1-2)")
     ap.add_argument("--pbas-gradient", action="store_true",
                     help="PBAS with the opt-in gradient feature (K2G; not the reference algorithm)")
     ap.add_argument("--stream-priority", type=int, default=0,

@@ -126,6 +126,17 @@ int rgbdseg_rng_keys(const uint64_t* keys_host, int64_t count, double* out_host,
  * (engine.py:60-72).  use_depth = (config.mode == "rgbd"). */
 int rgbdseg_gmm_create(int32_t width, int32_t height, const rgbdseg_gmm_params* params,
                        int32_t use_depth, int32_t device, rgbdseg_gmm** out);
+/* Same, with creation flags (no reference counterpart; 0 == rgbdseg_gmm_create):
+ *   RGBDSEG_GMM_STATE_F32  opt-in f32 state storage (SURVEY.md §8(d) "GMM 7/3
+ *       f32-storage", 245 instead of 485 B/px at 7/3): loads widen to f64,
+ *       the update runs the reference's f64 expressions, stores round to
+ *       nearest f32.  Masks / state stay within the north_star tolerance of
+ *       the f64 reference (>= 99.99 % of mask pixels, state 1e-5 relative,
+ *       tests/test_gmm_f32.py); read/write_state still exchange f64 in the
+ *       reference layout (writes round to f32). */
+#define RGBDSEG_GMM_STATE_F32 1u
+int rgbdseg_gmm_create_ex(int32_t width, int32_t height, const rgbdseg_gmm_params* params,
+                          int32_t use_depth, int32_t device, uint32_t flags, rgbdseg_gmm** out);
 void rgbdseg_gmm_destroy(rgbdseg_gmm* h);
 
 /* One frame, device buffers: GmmState.segment_rows over all rows

@@ -149,8 +149,14 @@ class OracleEngine:
         self.use_depth = config.mode == "rgbd"
         self.workers = workers if workers is not None else getattr(config, "workers", 1)
         self.gradient = None
+        # opt-in f32 GMM storage (package extension, csrc/gmm.cu StF32): every
+        # stored value rounded to nearest f32 -- rounding the whole state after
+        # each frame is the same rule, since pixels are independent and values
+        # the frame did not touch are already f32-representable
+        self.gmm_f32 = getattr(config, "gmm_state_dtype", "float64") == "float32"
         if config.algorithm == "gmm":
             self.state = gmm_state(width, height, config.gmm)
+            self._round_f32()
         else:
             self.state = pbas_state(width, height, config.pbas)
             self.gradient = getattr(config, "pbas_gradient", None)
@@ -160,6 +166,11 @@ class OracleEngine:
 
     def state_arrays(self) -> dict:
         return self.state
+
+    def _round_f32(self):
+        if self.gmm_f32:
+            for v in self.state.values():
+                v[...] = v.astype(np.float32).astype(np.float64)
 
     def process_frame(self, frame: np.ndarray) -> np.ndarray:
         frame = np.ascontiguousarray(frame, dtype=np.uint8)
@@ -176,6 +187,7 @@ class OracleEngine:
                 p.k_rgb, p.k_d, p.alpha, p.s, p.tau, p.match_lambda * p.match_lambda,
                 p.var_init, p.w_init, int(self.use_depth), _p(mask), self.workers)
             assert rc == 0
+            self._round_f32()
         else:
             p = self.config.pbas
             args = (self.width, self.height, _p(frame), self.frame_idx,

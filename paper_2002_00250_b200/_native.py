@@ -22,7 +22,7 @@ LIB_PATH = Path(os.environ.get("RGBDSEG_B200_LIB") or
 EXPORTS = (
     "rgbdseg_last_error", "rgbdseg_abi_version", "rgbdseg_device_count",
     "rgbdseg_rng_stream", "rgbdseg_rng_keys",
-    "rgbdseg_gmm_create", "rgbdseg_gmm_destroy", "rgbdseg_gmm_step", "rgbdseg_gmm_step_batch",
+    "rgbdseg_gmm_create", "rgbdseg_gmm_create_ex", "rgbdseg_gmm_destroy", "rgbdseg_gmm_step", "rgbdseg_gmm_step_batch",
     "rgbdseg_gmm_process_host", "rgbdseg_gmm_sync", "rgbdseg_gmm_state_bytes",
     "rgbdseg_gmm_read_state", "rgbdseg_gmm_write_state", "rgbdseg_gmm_stream",
     "rgbdseg_pbas_create", "rgbdseg_pbas_create_band", "rgbdseg_pbas_destroy",
@@ -42,6 +42,7 @@ EXPORTS = (
 
 IPC_HANDLE_BYTES = 64  # RGBDSEG_IPC_HANDLE_BYTES
 
+GMM_STATE_F32 = 1  # RGBDSEG_GMM_STATE_F32
 GMM_FIELDS = {"rgb_w": 0, "rgb_mu": 1, "rgb_var": 2, "d_w": 3, "d_mu": 4, "d_var": 5}
 PBAS_FIELDS = {"samples": 0, "dmin_rgb": 1, "dmin_d": 2, "len_rgb": 3, "pos_rgb": 4,
                "len_d": 5, "pos_d": 6, "r_rgb": 7, "r_d": 8, "t": 9,
@@ -79,6 +80,8 @@ def _declare(L):
         "rgbdseg_rng_stream": (ctypes.c_int, [u64, u64, u64, u64, i64, vp, i32]),
         "rgbdseg_rng_keys": (ctypes.c_int, [vp, i64, vp, i32]),
         "rgbdseg_gmm_create": (ctypes.c_int, [i32, i32, P(GmmParamsC), i32, i32, P(vp)]),
+        "rgbdseg_gmm_create_ex": (ctypes.c_int, [i32, i32, P(GmmParamsC), i32, i32, ctypes.c_uint32,
+                                                 P(vp)]),
         "rgbdseg_gmm_destroy": (None, [vp]),
         "rgbdseg_gmm_step": (ctypes.c_int, [vp, vp, vp, vp]),
         "rgbdseg_gmm_step_batch": (ctypes.c_int, [vp, i32, vp, vp, vp]),

@@ -87,7 +87,7 @@ class _Handle:
     """Owns one C-ABI handle (GMM or PBAS)."""
 
     def __init__(self, algorithm, width, height, params, use_depth, seed, device,
-                 band=None):
+                 band=None, gmm_flags=0):
         L = _native.lib()
         self.L = L
         self.algorithm = algorithm
@@ -97,8 +97,8 @@ class _Handle:
                               f"({_native.device_count()} visible); the B200 path has no CPU fallback")
         if algorithm == "gmm":
             self.pc = _native.gmm_params_c(params)
-            rc = L.rgbdseg_gmm_create(width, height, ctypes.byref(self.pc), int(use_depth),
-                                      device, ctypes.byref(self.ptr))
+            rc = L.rgbdseg_gmm_create_ex(width, height, ctypes.byref(self.pc), int(use_depth),
+                                         device, gmm_flags, ctypes.byref(self.ptr))
             _native.check(rc, "rgbdseg_gmm_create")
             self.pre = "rgbdseg_gmm_"
         else:
@@ -168,8 +168,10 @@ class SegmentationEngine:
         self.rows = self.height if _band is None else _band[1] - _band[0]
         params = config.gmm if config.algorithm == "gmm" else config.pbas
         self._params = params
+        self.gmm_state_dtype = getattr(config, "gmm_state_dtype", "float64")
+        gmm_flags = _native.GMM_STATE_F32 if self.gmm_state_dtype == "float32" else 0
         self._h = _Handle(config.algorithm, self.width, self.height, params, self.use_depth,
-                          config.seed, self.device, band=_band)
+                          config.seed, self.device, band=_band, gmm_flags=gmm_flags)
         self._gmm_frame_idx = 0
         self.gradient = getattr(config, "pbas_gradient", None) if config.algorithm == "pbas" else None
         if self.gradient is not None:  # opt-in extension, K2G (csrc/pbas.cu)
