@@ -573,6 +573,17 @@ def test_fast_divide_matches_ieee_divide_on_device():
     guard = rng.uniform(1.0, 255.0, m)
     num = np.where(rng.random(m) < 0.5, 1.0, -0.05) * 10.0 ** rng.uniform(-3, 3, m)
     check(num, guard, "t_step/guard")
+    # GMM renormalisation w / total (gmm.py:339-343; csrc/gmm.cu rcp_rn_f64 +
+    # div_by_rcp = this sequence with the reciprocal hoisted): weights in
+    # [1e-140, 1] (or 0), totals in [1e-3, 1.1], and the reference's
+    # renormalisation of freshly blended weight vectors
+    wts = rng.random(m) * 10.0 ** rng.uniform(-140, 0, m)
+    wts[rng.random(m) < 0.05] = 0.0
+    check(wts, rng.uniform(1e-3, 1.1, m), "w/total")
+    k = 7
+    wv = rng.dirichlet(np.ones(k), m // k) * (1.0 - 0.001)
+    wv[:, 0] += 0.001
+    check(wv.ravel(), np.repeat(wv.sum(axis=1), k), "blended weights / their sum")
     a = 10.0 ** rng.uniform(-145, 145, m) * np.where(rng.random(m) < 0.5, 1.0, -1.0)
     b = 10.0 ** rng.uniform(-145, 145, m)
     check(a, b, "log-uniform")
