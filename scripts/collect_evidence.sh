@@ -4,6 +4,7 @@ cd "$(dirname "$0")/.."
 P=profiles/r01
 cp gpurun_out/bench.json $P/final_bench.json
 cp gpurun_out/bench_ref.json $P/final_bench_ref.json
+cp gpurun_out/bench_gmm_f32.json $P/final_bench_gmm_f32.json
 for c in 1 2 3 4 5; do cp gpurun_out/cfg_config$c.json $P/configs/cfg_config$c.json; done
 cp gpurun_out/cfg_config5.json $P/final_bench_c5.json
 cp gpurun_out/launches.csv $P/launches_final.csv
