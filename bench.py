@@ -201,7 +201,7 @@ def _throttled(clock_info, dev, world) -> bool:
 def _pci_bus_id(dev) -> str | None:
     try:
         p = torch.cuda.get_device_properties(dev)
-        return f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        return f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
     except Exception:
         return None
 
