@@ -162,8 +162,9 @@ def test_gpu_f32_within_tolerance_of_reference_golden(name):
 
 @pytest.mark.gpu
 def test_gpu_f32_batched_equals_single_and_state_roundtrip():
-    from paper_2002_00250_b200.engine import MultiStreamEngine, SegmentationEngine
     import torch
+
+    from paper_2002_00250_b200.engine import MultiStreamEngine, SegmentationEngine, torch_stream_handle
 
     w, h, n = 64, 48, 3
     cfg = _f32(PipelineConfig(algorithm="gmm", gmm=GmmParams(k_rgb=7, k_d=3)))
@@ -173,7 +174,7 @@ def test_gpu_f32_batched_equals_single_and_state_roundtrip():
     for t in range(12):
         fr = [torch.from_numpy(seqs[i][t]).cuda() for i in range(n)]
         ms.step_ptrs([f.data_ptr() for f in fr], [masks[i].data_ptr() for i in range(n)],
-                     torch.cuda.current_stream().cuda_stream)
+                     torch_stream_handle())
     torch.cuda.synchronize()
     for i in range(n):
         m1, st1 = _gpu_run(cfg, seqs[i])
