@@ -511,12 +511,15 @@ def run_ours(args, rank, world, local_rank):
     tfile = ROOT / "profiles" / "traffic.json"
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get(f"{dom}:{args.workload}")
+            tkey = dom + ("_f32" if dom == "gmm" and args.gmm_state == "f32" else
+                          "_grad" if dom == "pbas" and args.pbas_gradient else "")
+            traffic = json.loads(tfile.read_text()).get(f"{tkey}:{args.workload}")
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "achieved": per_algo[dom].get("achieved_gbs"), "peak": peak,
             "unit": "GB/s", "frac": per_algo[dom].get("roofline_frac"), "traffic": traffic,
-            "kernel": "gmm_step_kernel<7,3> (K1)" if dom == "gmm" else "pbas_classify_kernel (K2)",
+            "kernel": (f"gmm_step_kernel<{gmm_k[0]},{gmm_k[1]},{'StF32' if args.gmm_state == 'f32' else 'StF64'}> (K1)"
+                       if dom == "gmm" else "pbas_classify_kernel (K2)"),
             "peak_kind": peak_kind,
             "bytes_per_launch_alg": (per_algo[dom]["bytes_per_pixel_alg"] or 0) * npix * S}
 
