@@ -189,3 +189,26 @@ def test_gpu_f32_batched_equals_single_and_state_roundtrip():
         eng.load_state(bumped)
         for k, v in eng.state_arrays().items():
             np.testing.assert_array_equal(v, bumped[k].astype(np.float32).astype(np.float64), err_msg=k)
+
+
+@pytest.mark.gpu
+def test_gpu_f32_match_gate_band_exact(oracle_mod):
+    """Observations exactly on / next to the match gate d2 = lam2 * v
+    (var_init = 4, lambda = 2.5: lam2 v = 25) so the FP32 gate's 2^-18 band
+    hands them to the f64 test; state must still equal the f32 oracle."""
+    w, h = 33, 7
+    rng = np.random.default_rng(11)
+    base = rng.integers(40, 200, size=(h, w, 4), dtype=np.uint8)
+    base[:, :, 3] = rng.integers(60, 190, size=(h, w))
+    offs = np.array([0, 5, 4, 6, 3, -5, 5, 0, 2, -4], dtype=np.int16)
+    frames = []
+    for t in range(24):
+        f = base.astype(np.int16).copy()
+        ch = t % 4
+        f[:, :, ch] += np.roll(offs, t)[np.arange(w) % len(offs)][None, :]
+        frames.append(np.clip(f, 0, 255).astype(np.uint8))
+    for mode in ("rgbd", "rgb_only"):
+        cfg = _f32(PipelineConfig(algorithm="gmm", mode=mode,
+                                  gmm=GmmParams(k_rgb=3, k_d=2, var_init=4.0, match_lambda=2.5,
+                                                alpha=0.25)))
+        _gpu_vs_f32_oracle(oracle_mod, cfg, frames)
