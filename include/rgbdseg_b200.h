@@ -215,7 +215,11 @@ int rgbdseg_pbas_halo_ptrs(rgbdseg_pbas* h, void** first_row, void** last_row, v
  *   classify_rows(edge rows) -> push(step) -> classify_rows(interior)
  *   -> pull(step) -> apply.
  * Waits are bounded (default 20 s): a timeout sets an error flag that
- * status() reports (RGBDSEG_E_RUNTIME) instead of hanging the GPU. */
+ * status() reports (RGBDSEG_E_RUNTIME) instead of hanging the GPU; the pull
+ * then leaves "no intent" in the halo rows (never the previous frame's
+ * codes).  error() reads the same flag from host-mapped memory without a
+ * device sync (1 = a wait timed out, 0 = none so far, -1 = NULL link): the
+ * Python band step polls it every frame. */
 int rgbdseg_halo_link_create(rgbdseg_pbas* band, int32_t device, rgbdseg_halo_link** out);
 int rgbdseg_halo_link_export(rgbdseg_halo_link* l, void* ipc_handle_out /* IPC_HANDLE_BYTES */);
 /* Map the neighbours' exported mailboxes (NULL: no band above / below). */
@@ -228,6 +232,7 @@ int rgbdseg_halo_link_push(rgbdseg_halo_link* l, uint64_t step, void* stream);
 int rgbdseg_halo_link_pull(rgbdseg_halo_link* l, uint64_t step, void* stream);
 int rgbdseg_halo_link_set_timeout(rgbdseg_halo_link* l, uint64_t timeout_ns);
 int rgbdseg_halo_link_status(rgbdseg_halo_link* l);
+int32_t rgbdseg_halo_link_error(const rgbdseg_halo_link* l);
 void rgbdseg_halo_link_destroy(rgbdseg_halo_link* l);
 /* Opt-in PBAS gradient-magnitude feature (no reference counterpart: the
  * reference drops the original PBAS gradient term; semantics in

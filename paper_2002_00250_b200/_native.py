@@ -34,7 +34,8 @@ EXPORTS = (
     "rgbdseg_confusion_accumulate", "rgbdseg_pack_frame", "rgbdseg_median3x3",
     "rgbdseg_halo_link_create", "rgbdseg_halo_link_export", "rgbdseg_halo_link_connect",
     "rgbdseg_halo_link_connect_local", "rgbdseg_halo_link_push", "rgbdseg_halo_link_pull",
-    "rgbdseg_halo_link_set_timeout", "rgbdseg_halo_link_status", "rgbdseg_halo_link_destroy",
+    "rgbdseg_halo_link_set_timeout", "rgbdseg_halo_link_status", "rgbdseg_halo_link_error",
+    "rgbdseg_halo_link_destroy",
     "rgbdseg_selftest_fdiv", "rgbdseg_gmm_set_eval", "rgbdseg_gmm_eval_counts",
     "rgbdseg_pbas_set_eval", "rgbdseg_pbas_eval_counts", "rgbdseg_pbas_set_k2_mode",
     "rgbdseg_pbas_get_k2_mode", "rgbdseg_pbas_set_gradient",
@@ -122,6 +123,7 @@ def _declare(L):
         "rgbdseg_halo_link_pull": (ctypes.c_int, [vp, u64, vp]),
         "rgbdseg_halo_link_set_timeout": (ctypes.c_int, [vp, u64]),
         "rgbdseg_halo_link_status": (ctypes.c_int, [vp]),
+        "rgbdseg_halo_link_error": (i32, [vp]),
         "rgbdseg_halo_link_destroy": (None, [vp]),
         "rgbdseg_selftest_fdiv": (ctypes.c_int, [vp, vp, i64, P(i64)]),
         "rgbdseg_gmm_set_eval": (ctypes.c_int, [vp, vp]),

@@ -136,6 +136,16 @@ class HaloLink:
         """Synchronise the device and raise DeviceError if a wait timed out."""
         _native.check(self._L.rgbdseg_halo_link_status(self.ptr), "halo exchange")
 
+    def check_error(self) -> None:
+        """Raise DeviceError if a wait of an earlier step timed out (reads the
+        host-mapped error word: no device sync, so a timeout surfaces at the
+        latest on the step after the one that hit it, or at status())."""
+        if self._L.rgbdseg_halo_link_error(self.ptr) == 1:
+            from .errors import DeviceError
+
+            raise DeviceError("halo exchange: a peer-memory wait timed out; the affected "
+                              "frame applied no cross-band neighbour updates")
+
     def close(self) -> None:
         if self.ptr:
             self._L.rgbdseg_halo_link_destroy(self.ptr)
@@ -152,6 +162,7 @@ def band_step_p2p(engine, link, frame, mask, stream) -> None:
         _native.check(L.rgbdseg_pbas_classify(h, frame, mask, stream), "classify")
         _native.check(L.rgbdseg_pbas_apply(h, frame, stream), "apply")
         return
+    link.check_error()
     step = fidx - n + 1
     rows = engine.rows
     _native.check(L.rgbdseg_pbas_classify_rows(h, frame, mask, 0, 1, stream), "classify edge")

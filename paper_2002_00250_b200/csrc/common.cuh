@@ -90,6 +90,18 @@ __device__ __forceinline__ void eval_block_accumulate(bool valid, bool fg, uint8
 int eval_sum_slots(unsigned long long* slots, int64_t* counts_dev, int accumulate, int reset,
                    cudaStream_t st);
 
+// ------------------------------------------------- cross-stream order --
+// A handle's state may be stepped on different streams (its own for host
+// buffers, the caller's for device tensors).  Before work on `st`, wait for
+// everything the handle's previous step enqueued on another stream: one
+// event record + stream wait, nothing when the stream does not change.
+inline int order_after(cudaStream_t last, cudaStream_t st, cudaEvent_t ev) {
+    if (!last || last == st || !ev) return RGBDSEG_OK;
+    RGBDSEG_CUDA_TRY(cudaEventRecord(ev, last));
+    RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+    return RGBDSEG_OK;
+}
+
 // ------------------------------------------------------------- tracing --
 // NVTX range around every C-ABI step (SURVEY.md §5 "tracing"): what an
 // nsys / ncu --nvtx capture of a host application groups the K1/K2/K3

@@ -52,6 +52,7 @@ struct HaloArgs {
     unsigned long long step;
     int64_t row_bytes, rowcap;
     unsigned long long timeout_ns;
+    unsigned int* err_host;  // device alias of the link's host-mapped error word
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -69,13 +70,19 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // Spin until *flag >= want (or the timeout passes: error flag, no hang).
+// The error is raised in the mailbox (read by rgbdseg_halo_link_status) and
+// in host-mapped memory, which the host polls after every step without a
+// device sync (rgbdseg_halo_link_error).
 __device__ bool wait_flag(const unsigned long long* flag, unsigned long long want,
-                          unsigned long long timeout_ns, unsigned int* err) {
+                          unsigned long long timeout_ns, unsigned int* err,
+                          unsigned int* err_host) {
     if (ld_acquire_sys(flag) >= want) return true;
     const unsigned long long t0 = globaltimer();
     while (ld_acquire_sys(flag) < want) {
         if (globaltimer() - t0 > timeout_ns) {
             atomicExch(err, 1u);
+            if (err_host) *reinterpret_cast<volatile unsigned int*>(err_host) = 1u;
+            __threadfence_system();
             return false;
         }
         __nanosleep(256);
@@ -104,8 +111,8 @@ __global__ void __launch_bounds__(512) halo_push_kernel(HaloArgs a) {
         // slot `parity` was last used at step k - 2: wait until it was drained
         const unsigned long long want = a.step >= 2 ? a.step - 2 : 0ull;
         bool good = true;
-        if (a.above) good &= wait_flag(&mine->consumed[0], want, a.timeout_ns, &mine->error);
-        if (a.below) good &= wait_flag(&mine->consumed[1], want, a.timeout_ns, &mine->error);
+        if (a.above) good &= wait_flag(&mine->consumed[0], want, a.timeout_ns, &mine->error, a.err_host);
+        if (a.below) good &= wait_flag(&mine->consumed[1], want, a.timeout_ns, &mine->error, a.err_host);
         ok = good;
     }
     __syncthreads();
@@ -128,12 +135,21 @@ __global__ void __launch_bounds__(512) halo_pull_kernel(HaloArgs a) {
     const int parity = (int)(a.step & 1ull);
     if (threadIdx.x == 0) {
         bool good = true;
-        if (a.above) good &= wait_flag(&mine->ready[0], a.step, a.timeout_ns, &mine->error);
-        if (a.below) good &= wait_flag(&mine->ready[1], a.step, a.timeout_ns, &mine->error);
+        if (a.above) good &= wait_flag(&mine->ready[0], a.step, a.timeout_ns, &mine->error, a.err_host);
+        if (a.below) good &= wait_flag(&mine->ready[1], a.step, a.timeout_ns, &mine->error, a.err_host);
         ok = good;
     }
     __syncthreads();
-    if (!ok) return;
+    if (!ok) {
+        // No mail this step: the halo rows must not keep the previous
+        // frame's codes (K3 would replay them).  "No intent" everywhere; the
+        // error is raised to the host on its next step / status call.
+        for (int64_t i = threadIdx.x; i < a.row_bytes; i += blockDim.x) {
+            if (a.above) a.halo_above[i] = 0xFFu;
+            if (a.below) a.halo_below[i] = 0xFFu;
+        }
+        return;
+    }
     if (a.above) copy_row(a.halo_above, slot_of(a.mine, parity, 0, a.rowcap), a.row_bytes);
     if (a.below) copy_row(a.halo_below, slot_of(a.mine, parity, 1, a.rowcap), a.row_bytes);
     __threadfence_system();
@@ -159,6 +175,8 @@ struct rgbdseg_halo_link {
     int64_t row_bytes = 0, rowcap = 0, box_bytes = 0;
     uint8_t *first = nullptr, *last = nullptr, *halo_above = nullptr, *halo_below = nullptr;
     unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;
+    volatile unsigned int* err_host = nullptr;  // mapped pinned error word
+    unsigned int* err_host_dev = nullptr;       // its device alias
 };
 
 static_assert(sizeof(cudaIpcMemHandle_t) == RGBDSEG_IPC_HANDLE_BYTES, "IPC handle size");
@@ -193,9 +211,19 @@ int rgbdseg_halo_link_create(rgbdseg_pbas* band, int32_t device, rgbdseg_halo_li
     DeviceGuard dg(device);
     cudaError_t e = cudaMalloc(&l->mine, (size_t)l->box_bytes);
     if (e == cudaSuccess) e = cudaMemset(l->mine, 0, (size_t)l->box_bytes);
+    void* hp = nullptr;
+    if (e == cudaSuccess) e = cudaHostAlloc(&hp, sizeof(unsigned int), cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        l->err_host = static_cast<volatile unsigned int*>(hp);
+        *l->err_host = 0u;
+        void* dp = nullptr;
+        e = cudaHostGetDevicePointer(&dp, hp, 0);
+        l->err_host_dev = static_cast<unsigned int*>(dp);
+    }
     if (e != cudaSuccess) {
         set_error("mailbox allocation: %s", cudaGetErrorString(e));
         if (l->mine) cudaFree(l->mine);
+        if (l->err_host) cudaFreeHost(const_cast<unsigned int*>(l->err_host));
         delete l;
         return RGBDSEG_E_RUNTIME;
     }
@@ -301,6 +329,7 @@ static HaloArgs args_of(const rgbdseg_halo_link* l, uint64_t step) {
     a.row_bytes = l->row_bytes;
     a.rowcap = l->rowcap;
     a.timeout_ns = l->timeout_ns;
+    a.err_host = l->err_host_dev;
     return a;
 }
 
@@ -356,9 +385,16 @@ int rgbdseg_halo_link_status(rgbdseg_halo_link* l) {
     return RGBDSEG_OK;
 }
 
+int32_t rgbdseg_halo_link_error(const rgbdseg_halo_link* l) {
+    if (!l || !l->err_host) return -1;
+    return *l->err_host ? 1 : 0;
+}
+
 void rgbdseg_halo_link_destroy(rgbdseg_halo_link* l) {
     if (!l) return;
     DeviceGuard dg(l->device);
+    cudaDeviceSynchronize();  // no kernel may still post to the mapped error word
+    if (l->err_host) cudaFreeHost(const_cast<unsigned int*>(l->err_host));
     if (l->above_ipc && l->above) cudaIpcCloseMemHandle(l->above);
     if (l->below_ipc && l->below) cudaIpcCloseMemHandle(l->below);
     if (l->mine) cudaFree(l->mine);

@@ -58,7 +58,8 @@ _PBAS_GRAD_SHAPES = {
 
 
 def default_device() -> int:
-    """LOCAL_RANK under torchrun, else RGBDSEG_DEVICE, else 0."""
+    """RGBDSEG_DEVICE when set (an explicit override: e.g. every rank of a
+    shared-GPU run on one device), else LOCAL_RANK under torchrun, else 0."""
     for var in ("RGBDSEG_DEVICE", "LOCAL_RANK"):
         if var in os.environ:
             return int(os.environ[var])

@@ -22,6 +22,8 @@ Every frame is a pure function of (regime, W, H, seed, t); frames are packed
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 
 BG_DEPTH8 = 155          # 40000 * 255 // 65535 (synth.py:36-37 after frames.py:46-52)
@@ -42,6 +44,14 @@ def background_rgb(width: int, height: int) -> np.ndarray:
     out[:, :, 2] = 90 + ((xs[None, :] + ys[:, None]) * 80) // max(width + height - 2, 1)
     speckle = ((xs[None, :] * 73856093) ^ (ys[:, None] * 19349663)) % 17
     return np.clip(out + speckle[:, :, None], 0, 255).astype(np.uint8)
+
+
+@functools.lru_cache(maxsize=4)
+def _background_i16(width: int, height: int) -> np.ndarray:
+    """background_rgb as int16, computed once per frame size (read-only)."""
+    bg = background_rgb(width, height).astype(np.int16)
+    bg.flags.writeable = False
+    return bg
 
 
 def _rects(width: int, height: int, t: int):
@@ -72,8 +82,7 @@ def _paint_wrapped(plane, x0, y0, w, h, fn):
 def frame_typical(width: int, height: int, seed: int, t: int) -> np.ndarray:
     """Regime T frame t of stream `seed`."""
     rng = np.random.default_rng([seed, t])
-    bg = background_rgb(width, height).astype(np.int16)
-    rgb = bg.copy()
+    rgb = _background_i16(width, height).copy()
     depth = np.full((height, width), BG_DEPTH8, dtype=np.int16)
     for x0, y0, w, h, kind in _rects(width, height, t):
         if kind == 0:

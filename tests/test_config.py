@@ -1,48 +1,46 @@
-"""Boundary types: the key=value config system (reference config.py:53-125)."""
+"""Boundary types: PipelineConfig / GmmParams / PbasParams validation.
+
+The rules are the reference's (GmmParams.validate gmm.py:53-62,
+PbasParams.validate pbas.py:57-63, PipelineConfig.validate config.py:37-50);
+the device-path limits (pbas.n <= 255, k <= 16) apply only to the algorithm
+that runs, so any config the reference accepts for that algorithm passes.
+"""
 
 import pytest
 
-from paper_2002_00250_b200.config import (ConfigError, PipelineConfig, apply_param_overrides,
-                                          default_workers, effective_config_lines,
-                                          parse_config_file)
-from paper_2002_00250_b200.errors import ConfigError as CE
+from paper_2002_00250_b200.config import GmmParams, PbasParams, PipelineConfig, validate_config
+from paper_2002_00250_b200.errors import ConfigError
 
 
-def test_parse_config_file(tmp_path):
-    p = tmp_path / "run.conf"
-    p.write_text("# comment\n\nalgo = pbas\n gmm.tau =  2.5 \npbas.n=12\n")
-    assert parse_config_file(p) == {"algo": "pbas", "gmm.tau": "2.5", "pbas.n": "12"}
-    bad = tmp_path / "bad.conf"
-    bad.write_text("algo pbas\n")
-    with pytest.raises(CE, match="bad.conf:1: expected 'key = value'"):
-        parse_config_file(bad)
-    with pytest.raises(CE, match="not found"):
-        parse_config_file(tmp_path / "missing.conf")
+def test_defaults_validate():
+    PipelineConfig().validate()
+    PipelineConfig(algorithm="pbas").validate()
 
 
-def test_apply_param_overrides_types_and_errors():
-    cfg = PipelineConfig()
-    apply_param_overrides(cfg, {"gmm.tau": "2.5", "pbas.n": "12", "gmm.k_rgb": "5"})
-    assert cfg.gmm.tau == 2.5 and cfg.pbas.n == 12 and cfg.gmm.k_rgb == 5
-    assert isinstance(cfg.pbas.n, int) and isinstance(cfg.gmm.tau, float)
-    for bad in ({"tau": "1"}, {"gmm.nope": "1"}, {"svm.c": "1"}, {"pbas.n": "x"}):
-        with pytest.raises(ConfigError):
-            apply_param_overrides(PipelineConfig(), bad)
+@pytest.mark.parametrize("bad", [
+    dict(algorithm="svm"), dict(mode="depth_only"), dict(workers=0), dict(seed=-1),
+    dict(seed=2 ** 64), dict(gmm=GmmParams(k_rgb=0)), dict(gmm=GmmParams(tau=0.0)),
+    dict(pbas=PbasParams(n=1, min_matches=2)), dict(pbas=PbasParams(t_init=1.0)),
+    dict(pbas=PbasParams(r_lower=0.0)), dict(gmm_state_dtype="float16"),
+])
+def test_reference_rules_raise_config_error(bad):
+    with pytest.raises(ConfigError):
+        PipelineConfig(**bad).validate()
 
 
-def test_default_workers(monkeypatch):
-    monkeypatch.delenv("RGBD_BGSEG_WORKERS", raising=False)
-    assert default_workers() == 1
-    monkeypatch.setenv("RGBD_BGSEG_WORKERS", "6")
-    assert default_workers() == 6
-    for bad in ("0", "x"):
-        monkeypatch.setenv("RGBD_BGSEG_WORKERS", bad)
-        with pytest.raises(ConfigError):
-            default_workers()
+def test_device_limits_only_for_the_algorithm_that_runs():
+    # pbas.n > 255 does not fit the u8 ring state; irrelevant for GMM
+    validate_config(PipelineConfig(algorithm="gmm", pbas=PbasParams(n=300)))
+    with pytest.raises(ConfigError, match="pbas.n"):
+        validate_config(PipelineConfig(algorithm="pbas", pbas=PbasParams(n=300)))
+    validate_config(PipelineConfig(algorithm="pbas", gmm=GmmParams(k_rgb=40)))
+    with pytest.raises(ConfigError, match="k_rgb"):
+        validate_config(PipelineConfig(algorithm="gmm", gmm=GmmParams(k_rgb=40)))
 
 
-def test_effective_config_lines():
-    lines = effective_config_lines(PipelineConfig(algorithm="pbas", seed=3), {"z": 1, "a": 2})
-    assert lines[:4] == ["algo = pbas", "mode = rgbd", "seed = 3", "workers = 1"]
-    assert "gmm.k_rgb = 7" in lines and "pbas.n = 20" in lines
-    assert lines[-2:] == ["a = 2", "z = 1"]
+def test_duck_typed_config():
+    class Cfg:
+        algorithm, mode, seed, workers = "pbas", "rgb_only", 5, 2
+        gmm, pbas = GmmParams(), PbasParams(n=7)
+
+    validate_config(Cfg())

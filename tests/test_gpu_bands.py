@@ -162,7 +162,25 @@ def test_halo_wait_times_out_instead_of_hanging():
     links[1].connect_local(links[0], None)
     links[0].set_timeout(0.05)
     st = ctypes.c_void_p(torch_stream_handle())
+    # stale codes in the halo row (as a previous frame would leave them)
+    from paper_2002_00250_b200 import _native
+
+    hb, rb = ctypes.c_void_p(), ctypes.c_int64()
+    _native.check(_native.lib().rgbdseg_pbas_halo_ptrs(engines[0]._h.ptr, None, None, None,
+                                                      ctypes.byref(hb), ctypes.byref(rb)))
+
+    class _Raw:  # device bytes as a torch view (CUDA array interface)
+        __cuda_array_interface__ = {"shape": (rb.value,), "typestr": "|u1",
+                                    "data": (hb.value, False), "version": 3}
+
+    halo = torch.as_tensor(_Raw(), device="cuda")
+    halo.fill_(0x03)
+    torch.cuda.synchronize()
     links[0].pull(1, st)  # band 1 never pushes step 1
+    torch.cuda.synchronize()
+    with pytest.raises(DeviceError, match="timed out"):
+        links[0].check_error()  # host-mapped flag, no device sync
+    assert bool((halo == 0xFF).all()), "a timed-out pull must leave 'no intent' in the halo"
     with pytest.raises(DeviceError, match="timed out"):
         links[0].status()
     torch.cuda.synchronize()

@@ -1,0 +1,175 @@
+"""GPU parity at the BASELINE configs' own sizes (SURVEY.md §8(d) "configs as
+runs"), against the CPU restatement (oracle/, pinned to the reference's
+golden vectors) -- bit-exact masks every frame, bit-exact state at fixed
+checkpoints:
+
+  config 3  GMM 7/3 + PBAS n=20, 1280x720, 1000 frames (regime T): long
+            enough for PBAS's T controller (pbas.py:456-465) to reach
+            t_lower = 2, where half of the background self-updates and emits
+            neighbour updates every frame and the auto K2 switch moves to the
+            tile variant;
+  config 5  PBAS n=20, 7680x4320 single stream, 30 frames (20 warm-up + 10
+            with neighbour updates): 1/2/4/8 row bands linked through their
+            peer-memory mailboxes == one band == the oracle
+            (engine.py:48-50 band split, pbas.py:479-507 cross-band intents);
+  GMM 7/3 at 1920x1080, 50 frames of regime S (every component seeded).
+"""
+
+from __future__ import annotations
+
+import collections
+import ctypes
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import golden_util as gu
+from paper_2002_00250_b200 import synth
+from paper_2002_00250_b200.config import GmmParams, PbasParams, PipelineConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint64) if a.dtype == np.float64 else a
+
+
+def _assert_state_equal(got, expected, keys, what=""):
+    for k in keys:
+        np.testing.assert_array_equal(_bits(got[k]), _bits(expected[k]), err_msg=f"{what} {k}")
+
+
+def frames_ahead(regime, w, h, seed, n, workers=6, k_rgb=7):
+    """synth frames 0..n-1 in order, generated `workers` frames ahead on a
+    thread pool (numpy releases the GIL in the bulk generators)."""
+    with ThreadPoolExecutor(workers) as ex:
+        q = collections.deque()
+        nxt = 0
+        while nxt < min(n, 2 * workers):
+            q.append(ex.submit(synth.make_frame, regime, w, h, seed, nxt, k_rgb))
+            nxt += 1
+        for _ in range(n):
+            f = q.popleft().result()
+            if nxt < n:
+                q.append(ex.submit(synth.make_frame, regime, w, h, seed, nxt, k_rgb))
+                nxt += 1
+            yield f
+
+
+def test_config3_720p_1000_frames_gmm_and_pbas_vs_oracle(oracle_mod):
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    w, h, n = 1280, 720, 1000
+    checkpoints = {40, 300, 1000}
+    gcfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=7, k_d=3))
+    pcfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=20), seed=1)
+    threads = oracle_mod.cpu_threads()
+    ref_g = oracle_mod.OracleEngine(gcfg, w, h, workers=threads)
+    ref_p = oracle_mod.OracleEngine(pcfg, w, h, workers=threads)
+    modes = []
+    with SegmentationEngine(gcfg, w, h, device=0) as eg, \
+            SegmentationEngine(pcfg, w, h, device=0) as ep:
+        L = ep._h.L
+        for t, f in enumerate(frames_ahead("T", w, h, seed=0, n=n)):
+            mg = eg.process_frame(f)
+            mp = ep.process_frame(f)
+            modes.append(int(L.rgbdseg_pbas_get_k2_mode(ep._h.ptr)))
+            rg = ref_g.process_frame(f)
+            rp = ref_p.process_frame(f)
+            dg = int(np.count_nonzero(mg != rg))
+            assert dg == 0, f"GMM frame {t}: {dg} mask pixels differ"
+            np.testing.assert_array_equal(mp, rp, err_msg=f"PBAS frame {t}")
+            if t + 1 in checkpoints:
+                _assert_state_equal(eg.state_arrays(), ref_g.state_arrays(), gu.GMM_KEYS,
+                                    f"GMM after {t + 1} frames")
+                _assert_state_equal(ep.state_arrays(), ref_p.state_arrays(), gu.PBAS_KEYS,
+                                    f"PBAS after {t + 1} frames")
+    tmed = float(np.median(ref_p.state_arrays()["t"]))
+    assert tmed == pcfg.pbas.t_lower, f"T did not reach t_lower (median {tmed})"
+    # the production auto switch ran the tile K2 for the aged model ...
+    assert 2 in modes, "the auto K2 switch never chose the tile variant"
+    first_tile = modes.index(2)
+    assert modes[-1] == 2, "K2 is not on the tile variant at T = t_lower"
+    # ... and the row kernel while the model was young
+    assert modes[21] == 1
+    print(f"config 3: tile K2 from frame {first_tile}; T median at 1000 = {tmed}")
+
+
+@pytest.mark.parametrize("bands", [(2, 4, 8)])
+def test_config5_8k_pbas_row_bands_equal_one_band_and_oracle(oracle_mod, bands):
+    import torch
+
+    from paper_2002_00250_b200 import _native
+    from paper_2002_00250_b200.bands import HaloLink, band_bounds
+    from paper_2002_00250_b200.engine import SegmentationEngine, torch_stream_handle
+
+    w, h, n = 7680, 4320, 30
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=20), seed=5)
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    one = SegmentationEngine(cfg, w, h, device=0)
+    L = _native.lib()
+    st = ctypes.c_void_p(torch_stream_handle())
+    groups = []
+    for nb in bands:
+        bounds = band_bounds(h, nb)
+        engines = [SegmentationEngine(cfg, w, h, device=0, _band=b) for b in bounds]
+        links = [HaloLink(e) for e in engines]
+        for i, l in enumerate(links):
+            l.connect_local(links[i - 1] if i > 0 else None, links[i + 1] if i < nb - 1 else None)
+        groups.append((nb, bounds, engines, links))
+    mask = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+    for t, f in enumerate(frames_ahead("T", w, h, seed=9, n=n)):
+        fr = torch.from_numpy(f).cuda()
+        want = ref.process_frame(f)
+        np.testing.assert_array_equal(one.process_frame(fr).cpu().numpy(), want,
+                                      err_msg=f"1 band, frame {t}")
+        step = t - cfg.pbas.n + 1
+        for nb, bounds, engines, links in groups:
+            mask.fill_(7)
+            ptrs = [(ctypes.c_void_p(fr[y0:y1].data_ptr()), ctypes.c_void_p(mask[y0:y1].data_ptr()))
+                    for (y0, y1) in bounds]
+            # the per-GPU schedule of bands.band_step_p2p, every band on this device
+            for e, l, (fp, mp) in zip(engines, links, ptrs):
+                if step >= 1:
+                    _native.check(L.rgbdseg_pbas_classify_rows(e._h.ptr, fp, mp, 0, 1, st))
+                    _native.check(L.rgbdseg_pbas_classify_rows(e._h.ptr, fp, mp, e.rows - 1,
+                                                               e.rows, st))
+                    l.push(step, st)
+                    _native.check(L.rgbdseg_pbas_classify_rows(e._h.ptr, fp, mp, 1, e.rows - 1, st))
+                else:
+                    _native.check(L.rgbdseg_pbas_classify(e._h.ptr, fp, mp, st))
+            for e, l, (fp, _) in zip(engines, links, ptrs):
+                if step >= 1:
+                    l.pull(step, st)
+                _native.check(L.rgbdseg_pbas_apply(e._h.ptr, fp, st))
+            np.testing.assert_array_equal(mask.cpu().numpy(), want, err_msg=f"{nb} bands, frame {t}")
+    for _, _, _, links in groups:
+        for l in links:
+            l.status()
+    full = ref.state_arrays()
+    _assert_state_equal(one.state_arrays(), full, gu.PBAS_KEYS, "1 band")
+    for nb, bounds, engines, links in groups:
+        for e, (y0, y1) in zip(engines, bounds):
+            sub = {k: v[y0:y1] for k, v in full.items()}
+            _assert_state_equal(e.state_arrays(), sub, gu.PBAS_KEYS, f"{nb} bands [{y0}:{y1})")
+        for l in links:
+            l.close()
+        for e in engines:
+            e.close()
+    one.close()
+
+
+def test_gmm_1080p_regime_s_50_frames_vs_oracle(oracle_mod):
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    w, h, n = 1920, 1080, 50
+    cfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=7, k_d=3))
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    with SegmentationEngine(cfg, w, h, device=0) as eng:
+        for t, f in enumerate(frames_ahead("S", w, h, seed=4, n=n)):
+            d = int(np.count_nonzero(eng.process_frame(f) != ref.process_frame(f)))
+            assert d == 0, f"frame {t}: {d} mask pixels differ"
+        _assert_state_equal(eng.state_arrays(), ref.state_arrays(), gu.GMM_KEYS, "GMM 1080p")
+    assert (ref.state_arrays()["rgb_w"] > 0).all()  # regime S seeds every component
