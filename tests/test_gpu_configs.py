@@ -86,15 +86,20 @@ def test_config3_720p_1000_frames_gmm_and_pbas_vs_oracle(oracle_mod):
                                     f"GMM after {t + 1} frames")
                 _assert_state_equal(ep.state_arrays(), ref_p.state_arrays(), gu.PBAS_KEYS,
                                     f"PBAS after {t + 1} frames")
-    tmed = float(np.median(ref_p.state_arrays()["t"]))
-    assert tmed == pcfg.pbas.t_lower, f"T did not reach t_lower (median {tmed})"
+    t_final = ref_p.state_arrays()["t"]
+    at_lower = float(np.mean(t_final == pcfg.pbas.t_lower))
+    tmed = float(np.median(t_final))
+    # oracle run of this sequence: 0 % of the pixels at t_lower after 500
+    # frames, 36 % after 600, 46 % after 1000 (T median 2.78)
+    assert at_lower >= 0.4, f"only {at_lower:.3f} of the pixels reached t_lower"
     # the production auto switch ran the tile K2 for the aged model ...
     assert 2 in modes, "the auto K2 switch never chose the tile variant"
     first_tile = modes.index(2)
     assert modes[-1] == 2, "K2 is not on the tile variant at T = t_lower"
     # ... and the row kernel while the model was young
     assert modes[21] == 1
-    print(f"config 3: tile K2 from frame {first_tile}; T median at 1000 = {tmed}")
+    print(f"config 3: tile K2 from frame {first_tile}; T median at 1000 = {tmed}, "
+          f"{at_lower:.3f} at t_lower")
 
 
 @pytest.mark.parametrize("bands", [(2, 4, 8)])
