@@ -17,6 +17,11 @@ w, h, S = 1920, 1080, 8
 dev = torch.device("cuda", 0)
 eng = MultiStreamEngine(PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=20)), w, h, S,
                         device=0, seeds=[i + 1 for i in range(S)])
+mode = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # K2 variant: 0 auto, 1 rows, 2 strips
+if mode:
+    from paper_2002_00250_b200 import _native  # noqa: E402
+    for e in eng.engines:
+        _native.check(_native.lib().rgbdseg_pbas_set_k2_mode(e._h.ptr, mode))
 ring = torch.from_numpy(_gen_ring("T", w, h, list(range(S)), 8)).to(dev)
 masks = torch.empty((S, h, w), dtype=torch.uint8, device=dev)
 R = ring.shape[1]
@@ -39,6 +44,6 @@ for m in marks:
     b.record()
     torch.cuda.synchronize()
     T = eng.engines[0].state_arrays()["t"]
-    out.append({"frame": m, "ms_per_frame": a.elapsed_time(b) / 50,
+    out.append({"mode": mode, "frame": m, "ms_per_frame": a.elapsed_time(b) / 50,
                 "T_median": float(np.median(T)), "T_p10": float(np.percentile(T, 10))})
     print(json.dumps(out[-1]), flush=True)
