@@ -16,19 +16,21 @@ ranks per second, each pixel segmented by both algorithms); weak scaling
 Inputs: SURVEY.md §8(d) regimes, generated untimed and uploaded to HBM as a
 frame ring per stream: GMM runs on regime S (every component seeded, so the
 algorithmic byte count is honest), PBAS on regime T (moving objects + depth
-holes).  The state is burned in before the warm-up steps (GMM: all 7/3
-components seeded; PBAS: 2n = 40 frames, dmin rings full).
-With the default --warmup 10 --steps 100 the timed frames are 100-200 of the
-200-frame BASELINE config-4 sequence.  PBAS's work per frame keeps growing
-with model age (update probability 1/T, T adapting down), so the
-line reports the timed window, T's median and the K2 variant (`model_age`).
-The per-step working set (5.8 GB GMM + 2.5 GB PBAS state per GPU) is far
-larger than L2, so no explicit flush is needed; smaller workloads (configs
-1-2) flush L2 between individually timed steps.
+holes).  The state is burned in before anything is timed: GMM 8 frames (all
+7/3 components seeded); PBAS --pbas-age frames (default 400), because its
+work per frame grows with model age (update probability 1/T, T adapting down
+to t_lower after ~300 frames) -- the timed window and the PBAS
+per_algo/roofline are at steady state (model_age: T median = t_lower), and
+frames 40-90 of the burn-in (young model, PBAS alone) are reported as
+`pbas_young`.  The per-step working set (5.8 GB GMM + 2.5 GB PBAS state per
+GPU) is far larger than L2, so no explicit flush is needed; smaller
+workloads (configs 1-2) flush L2 between individually timed steps.
 
 Extra keys: roofline (GMM K1, the dominant kernel), per-algorithm breakdown,
 cpu_baseline (the oracle port on this host's cores), e2e (the public
-SegmentationEngine host-buffer path with H2D/D2H inside the timed region),
+host-buffer APIs with H2D/D2H inside the timed region: MultiCameraPipeline
+with one shared upload per camera frame, and e2e.dropin = the reference's
+per-frame SegmentationEngine.process_frame(numpy) call on one stream),
 clocks (nvidia-smi sampled during the timed region), gpu_launches.
 
 `--impl reference` times the reference algorithm's CPU implementation (the
@@ -192,6 +194,9 @@ def _throttled(clock_info, dev, world) -> bool:
     bad = bool(clock_info and set(clock_info["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown",
                                                             "sw_thermal_slowdown"})
     if world > 1:
+        import torch
+        import torch.distributed as dist
+
         flag = torch.tensor([int(bad)], device=dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MAX)
         bad = bool(flag.item())
@@ -219,6 +224,10 @@ def _native_k2_mode(ms_engine) -> int:
     from paper_2002_00250_b200 import _native
 
     return int(_native.lib().rgbdseg_pbas_get_k2_mode(ms_engine.engines[0]._h.ptr))
+
+
+def _k2_name(ms_engine) -> str:
+    return "strips" if _native_k2_mode(ms_engine) == 2 else "rows"
 
 
 def _cpu_model() -> str:
@@ -392,12 +401,32 @@ def run_ours(args, rank, world, local_rank):
             if args.flush == "write+read":
                 flush_buf.amax()
 
-    burn = max([8 if a[0] == "gmm" else 2 * pbas_n for a in algos])
+    # Burn-in.  GMM: 8 frames seed every component.  PBAS: its per-frame
+    # work grows with model age (update probability 1/T, T adapting down to
+    # t_lower over ~300 frames of the synthetic scene), so it is
+    # aged to steady state (--pbas-age frames, T = t_lower) before anything
+    # is timed; frames 40-90 of the burn-in (young model, PBAS alone) are
+    # timed on the way and reported as `pbas_young`.
+    burn_of = {a[0]: (8 if a[0] == "gmm" else max(2 * pbas_n, args.pbas_age)) for a in algos}
+    burn = max(burn_of.values())
+    young = None
+    yw = (2 * pbas_n, 2 * pbas_n + 50) if pbas_n else None
+    ev_y = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
     for t in range(burn):
+        if yw and "pbas" in streams and burn_of["pbas"] >= yw[1] and t in yw:
+            ev_y[yw.index(t)].record(streams["pbas"])
+            if t == yw[1]:
+                torch.cuda.synchronize()
+                pe = next(a[1] for a in algos if a[0] == "pbas")
+                tt = pe.engines[0].state_arrays()["t"]
+                ms_y = ev_y[0].elapsed_time(ev_y[1]) / (yw[1] - yw[0])
+                young = {"frames": list(yw), "pbas_T_median": float(np.median(tt)),
+                         "ms_per_step": ms_y, "k2_variant": _k2_name(pe)}
         for name, eng, ring, _ in algos:
-            launch(name, eng, ring, t)
+            if t < burn_of[name]:
+                launch(name, eng, ring, t)
     torch.cuda.synchronize()
-    t_frame = burn
+    t_frame_by = dict(burn_of)
 
     # ---- solo phase: each algorithm alone, per-launch CUDA events on its own
     # stream -> the per-kernel durations the roofline is computed from.
@@ -406,6 +435,7 @@ def run_ours(args, rank, world, local_rank):
     per_algo_ms = {}
     for name, eng, ring, _ in algos:
         st = streams[name]
+        t_frame = t_frame_by[name]
         if flush_buf is None:
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(solo + 1)]
             for k in range(solo):
@@ -427,9 +457,7 @@ def run_ours(args, rank, world, local_rank):
                     t_frame += 1
             torch.cuda.synchronize()
             per_algo_ms[name] = [a.elapsed_time(b) for a, b in pairs]
-    # the solo steps advanced each engine's stream by `solo` frames; keep the
-    # engines in lock-step for the concurrent phase
-    t_frame_by = {a[0]: t_frame for a in algos}
+        t_frame_by[name] = t_frame
 
     # ---- warm-up + timed region (concurrent schedule)
     def step():
@@ -525,15 +553,22 @@ def run_ours(args, rank, world, local_rank):
 
     # PBAS's per-frame work grows with model age (update probability 1/T, T
     # adapting down): report the timed frame window and T then.
-    done = int(algos[0][1].engines[0].frame_idx)  # frames each engine has segmented
-    age_info = {"timed_frames": [done - args.steps, done]}
+    age_info = {}
     for name, eng, _, _ in algos:
+        done = t_frame_by[name]  # frames this engine has segmented
+        age_info[f"{name}_timed_frames"] = [done - args.steps, done]
+        age_info[f"{name}_solo_frames"] = [done - args.steps - args.warmup - solo,
+                                           done - args.steps - args.warmup]
         if name == "pbas":
-            import numpy as np
-
             tt = eng.engines[0].state_arrays()["t"]
             age_info.update({"pbas_T_median": float(np.median(tt)),
-                             "pbas_k2_variant": ("tiles" if _native_k2_mode(eng) == 2 else "rows")})
+                             "pbas_T_at_t_lower": float(np.mean(tt == eng.config.pbas.t_lower)),
+                             "pbas_k2_variant": _k2_name(eng)})
+    if young is not None:
+        peak_y, _ = measured_peaks()
+        balg = B_ALG.get(("pbas_grad" if args.pbas_gradient else "pbas", pbas_n))
+        gbs = balg * npix * S / (young["ms_per_step"] / 1e3) / 1e9
+        young.update({"achieved_gbs": gbs, "roofline_frac": gbs / peak_y})
 
     # ---- e2e through the public host-buffer API (rank-local, then max)
     e2e = None
@@ -576,7 +611,7 @@ def run_ours(args, rank, world, local_rank):
                        "pbas_gradient": ({"alpha": PbasGradient().alpha,
                                           "mean_init": PbasGradient().mean_init}
                                          if args.pbas_gradient else None),
-                       "burn_in_frames": burn,
+                       "burn_in_frames": burn_of,
                        "l2": (f"inputs larger than L2 (state per step {state_bytes / 1e9:.2f} GB "
                               f">> {l2_bytes >> 20} MB)" if flush_buf is None else
                               f"L2 flushed between timed steps ({2 * l2_bytes >> 20} MB {args.flush}, "
@@ -585,7 +620,8 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"streams sharded {S}/GPU over {world} GPU(s)",
                        "schedule": "GMM and PBAS engines on two CUDA streams, concurrently "
                                    f"(PBAS priority +{args.stream_priority}); per_algo/roofline "
-                                   "from a solo phase of each"},
+                                   "from a solo phase of each right before the timed window "
+                                   "(same model age: PBAS at steady state, T = t_lower)"},
             "fps": fps,
             "per_algo": per_algo,
             "roofline": roof,
@@ -595,6 +631,7 @@ def run_ours(args, rank, world, local_rank):
             "clocks": (dict(clock_info, remeasured=remeasured) if clock_info else None),
             "fg_fraction_last_step": float(counters[0].item()) / float(counters[1].item()),
             "model_age": age_info,
+            "pbas_young": young,
         }
         print(json.dumps(line), flush=True)
     for _, eng, _, _ in algos:
@@ -682,32 +719,96 @@ def run_config5(args, rank, world, local_rank):
 
 
 def run_e2e(args, algos, S, w, h, dev, world):
-    """Same workload through the public host-buffer API: MultiCameraPipeline
-    (pipeline.py) over the already burned-in engines.  Every step copies each
-    camera's frame(s) H2D from pinned memory and every mask D2H, inside the
-    timed region; steps are double-buffered so copies overlap compute.  The
-    algorithms keep their own inputs (regime S for GMM, T for PBAS), so each
-    frame is uploaded once per algorithm, as in the device-resident run."""
+    """The same workload end to end through the public host-buffer APIs,
+    H2D of the inputs and D2H of the masks inside the timed region:
+
+      shared   pipeline.MultiCameraPipeline over the burned-in engines: each
+               step uploads ONE (S, H, W, 4) batch of camera frames from
+               pinned memory, shared by GMM and PBAS (4 B/px in), and
+               downloads both masks (2 B/px out); double-buffered so step
+               t+1's upload overlaps step t's kernels;
+      dropin   SegmentationEngine.process_frame(numpy) -- the reference's
+               per-frame call (engine.py:99-112; process_sequence and the
+               service use it): one 1920x1080 stream, pageable numpy frame
+               in, numpy mask out, GMM engine then PBAS engine per frame
+               (each call synchronous, staged through the handle's pinned
+               buffers in chunks)."""
     import torch
     import torch.distributed as dist
 
+    from paper_2002_00250_b200.engine import SegmentationEngine
     from paper_2002_00250_b200.pipeline import MultiCameraPipeline
 
     npix = w * h
     steps = max(3, args.e2e_steps)  # pipeline fill + drain amortised over the steps
-    pipe = MultiCameraPipeline({}, w, h, S, device=dev.index, engines={a[0]: a[1] for a in algos})
-    host_in = {}
+    # One camera-frame stream shared by every algorithm (regime T; --e2e-input
+    # S for the saturated one).  The PBAS engines are already at steady state
+    # on regime T; GMM gets its own engines burned in on the same frames (the
+    # bench's GMM state is trained on regime S, and switching the scene under
+    # it would time a scene change, not a steady camera).
+    src = next((a[2] for a in algos if a[0] == ("gmm" if args.e2e_input == "S" else "pbas")),
+               algos[0][2])
+    R = src.shape[1]
+    engines, owned = {}, []
     for name, eng, ring, _ in algos:
-        pinned = torch.empty((ring.shape[1],) + tuple(ring.shape[:1]) + tuple(ring.shape[2:]),
-                             dtype=torch.uint8, pin_memory=True)
-        pinned.copy_(ring.transpose(0, 1))  # (R, S, H, W, 4): one batch per step
-        host_in[name] = pinned
-    host_out = [{a[0]: torch.empty((S, h, w), dtype=torch.uint8, pin_memory=True) for a in algos}
+        if ring is src:
+            engines[name] = eng
+            continue
+        from paper_2002_00250_b200.engine import MultiStreamEngine
+
+        fresh = MultiStreamEngine(eng.config, w, h, S, device=dev.index,
+                                  seeds=[e.config.seed for e in eng.engines])
+        owned.append(fresh)
+        engines[name] = fresh
+    cs = {name: torch.cuda.Stream(dev) for name in engines}
+    dmask = torch.empty((S, h, w), dtype=torch.uint8, device=dev)
+
+    def dev_step(name, t):
+        base = src.data_ptr()
+        engines[name].step_ptrs([base + ((i * R) + (t % R)) * npix * 4 for i in range(S)],
+                                [dmask.data_ptr() + i * npix for i in range(S)], cs[name].cuda_stream)
+
+    for e in owned:  # burn-in of the fresh engines on the shared frames
+        name = next(k for k, v in engines.items() if v is e)
+        for t in range(50):
+            dev_step(name, t)
+    torch.cuda.synchronize()
+    # device-resident rate on the same shared input (the e2e leg's ceiling)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    first = next(iter(cs.values()))
+    ev0.record(first)
+    for q in cs.values():
+        q.wait_event(ev0)
+    for t in range(30):
+        for name in engines:
+            dev_step(name, t)
+    for q in cs.values():
+        e_ = torch.cuda.Event()
+        e_.record(q)
+        first.wait_event(e_)
+    ev1.record(first)
+    torch.cuda.synchronize()
+    dev_ms = ev0.elapsed_time(ev1) / 30
+    pipe = MultiCameraPipeline({}, w, h, S, device=dev.index, engines=engines)
+    pinned = torch.empty((R, S, h, w, 4), dtype=torch.uint8, pin_memory=True)
+    pinned.copy_(src.transpose(0, 1))  # (R, S, H, W, 4): one batch per step
+    host_out = [{name: torch.empty((S, h, w), dtype=torch.uint8, pin_memory=True) for name in engines}
                 for _ in range(pipe.depth)]
 
     def step(t):
-        return pipe.submit({a[0]: host_in[a[0]][t % host_in[a[0]].shape[0]] for a in algos},
-                           host_out[t % pipe.depth])
+        return pipe.submit(pinned[t % R], host_out[t % pipe.depth])
+
+    # pinned H2D rate of this box (the leg's other ceiling: 4 B/px in)
+    scratch = torch.empty_like(pinned[0], device=dev)
+    scratch.copy_(pinned[0], non_blocking=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(10):
+        scratch.copy_(pinned[k % R], non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = 10 * scratch.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del scratch
 
     for t in range(3):
         step(t)
@@ -724,12 +825,57 @@ def run_e2e(args, algos, S, w, h, dev, world):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     dt = float(tt.item())
-    return {"value": npix * S * world * steps / dt / 1e6, "unit": UNIT,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": npix * S * len(algos),
-            "steps": steps,
-            "timing": "host perf_counter from first submit to final synchronize (spans H2D+D2H)",
-            "api": "pipeline.MultiCameraPipeline.submit (pinned host buffers, double-buffered, "
-                   "copy-in / per-algorithm compute / copy-out streams)"}
+    out = {"value": npix * S * world * steps / dt / 1e6, "unit": UNIT,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": npix * S * len(algos),
+           "steps": steps,
+           "timing": "host perf_counter from first submit to final synchronize (spans H2D+D2H)",
+           "api": "pipeline.MultiCameraPipeline.submit: one shared pinned upload per camera frame "
+                  "for all algorithms, double-buffered copy-in / per-algorithm compute / copy-out "
+                  "streams",
+           "input": f"regime {args.e2e_input} camera frames shared by both algorithms",
+           "device_resident_same_input": {
+               "ms_per_step": dev_ms, "value": npix * S * world / (dev_ms / 1e3) / 1e6,
+               "note": "the same engines and frames with no host copies (the leg's ceiling)"},
+           "pcie_h2d_gbs": h2d_gbs,
+           "pcie_bound_value": h2d_gbs * 1e9 / 4 * world / 1e6}
+    for e in owned:
+        e.close()
+
+    # ---- drop-in leg: the reference's per-frame call on one stream
+    gmm_k = next((a[1].config.gmm for a in algos if a[0] == "gmm"), None)
+    pbas_p = next((a[1].config.pbas for a in algos if a[0] == "pbas"), None)
+    engines = []
+    if gmm_k is not None:
+        engines.append(SegmentationEngine(PipelineConfig(algorithm="gmm", mode="rgbd", gmm=gmm_k),
+                                          w, h, device=dev.index))
+    if pbas_p is not None:
+        engines.append(SegmentationEngine(PipelineConfig(algorithm="pbas", mode="rgbd", pbas=pbas_p,
+                                                         seed=1), w, h, device=dev.index))
+    frames = [np.ascontiguousarray(src[0, k].cpu().numpy()) for k in range(min(8, src.shape[1]))]
+    for t in range(2 * (pbas_p.n if pbas_p else 4) + 5):
+        for e in engines:
+            e.process_frame(frames[t % len(frames)])
+    nd = max(10, args.e2e_steps)
+    t0 = time.perf_counter()
+    for t in range(nd):
+        for e in engines:
+            e.process_frame(frames[t % len(frames)])
+    dt = time.perf_counter() - t0
+    for e in engines:
+        e.close()
+    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    dt = float(tt.item())
+    out["dropin"] = {"value": npix * world * nd / dt / 1e6, "unit": UNIT,
+                     "ms_per_frame": dt / nd * 1e3, "frames": nd,
+                     "h2d_bytes_per_step": 4 * npix * len(engines),
+                     "d2h_bytes_per_step": npix * len(engines),
+                     "api": "SegmentationEngine.process_frame(numpy) -> numpy, one stream per rank, "
+                            + " then ".join(e.config.algorithm.upper() for e in engines)
+                            + " engine per frame (synchronous; pageable numpy in/out)",
+                     "timing": "host perf_counter over the frames"}
+    return out
 
 
 def main():
@@ -751,6 +897,10 @@ def main():
     ap.add_argument("--stream-priority", type=int, default=0,
                     help="PBAS stream priority boost over GMM (0 = equal)")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--e2e-input", choices=["T", "S"], default="T",
+                    help="camera frames of the shared-upload e2e leg (regime T or S)")
+    ap.add_argument("--pbas-age", type=int, default=400,
+                    help="PBAS burn-in frames before timing (400: T at t_lower, steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",

@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <string>
 #include <utility>
 
@@ -101,6 +102,134 @@ inline int order_after(cudaStream_t last, cudaStream_t st, cudaEvent_t ev) {
     RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
     return RGBDSEG_OK;
 }
+
+// ------------------------------------------------ host-buffer staging --
+// The drop-in host path (process_frame(numpy): engine.py:99-112 returns the
+// mask of THIS frame) and the asynchronous submit() path, per handle:
+//   * two device slots (frame + mask), so frame t+1's upload (copy-in stream)
+//     overlaps frame t's kernels (handle stream) and frame t-1's download
+//     (copy-out stream); all ordering by events;
+//   * sync: the caller's pageable buffer is copied into a page-locked staging
+//     buffer in chunks on the calling thread, each chunk's DMA enqueued as
+//     soon as it is staged (host copy of chunk i+1 overlaps the DMA of chunk
+//     i), and the mask comes back the same way (DMA of chunk j+1 overlaps the
+//     host copy of chunk j) -- no pageable cudaMemcpy (driver bounce
+//     buffers, ~19 GB/s) and no hidden synchronisation;
+//   * async: the caller's buffers (pinned, alive until sync) are DMA'd
+//     directly.
+struct HostStaging {
+    static constexpr int IN_CHUNKS = 8, OUT_CHUNKS = 4;
+    int64_t in_bytes = 0, out_bytes = 0;
+    uint8_t* pin_in = nullptr;
+    uint8_t* pin_out = nullptr;
+    uint8_t* dev_in[2] = {nullptr, nullptr};
+    uint8_t* dev_out[2] = {nullptr, nullptr};
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t in_ready[2] = {}, step_done[2] = {}, out_done[2] = {}, out_chunk[OUT_CHUNKS] = {};
+    bool used[2] = {false, false};
+    int slot = 0;
+
+    int ensure(int64_t ib, int64_t ob) {
+        if (pin_in) return RGBDSEG_OK;
+        in_bytes = ib;
+        out_bytes = ob;
+        RGBDSEG_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&pin_in), ib, cudaHostAllocDefault));
+        RGBDSEG_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&pin_out), ob, cudaHostAllocDefault));
+        for (int i = 0; i < 2; ++i) {
+            RGBDSEG_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dev_in[i]), ib));
+            RGBDSEG_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dev_out[i]), ob));
+            RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming));
+            RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&step_done[i], cudaEventDisableTiming));
+            RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming));
+        }
+        for (int j = 0; j < OUT_CHUNKS; ++j)
+            RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&out_chunk[j], cudaEventDisableTiming));
+        RGBDSEG_CUDA_TRY(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+        RGBDSEG_CUDA_TRY(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+        return RGBDSEG_OK;
+    }
+
+    void release() {
+        if (s_in) cudaStreamSynchronize(s_in);
+        if (s_out) cudaStreamSynchronize(s_out);
+        for (int i = 0; i < 2; ++i) {
+            if (dev_in[i]) cudaFree(dev_in[i]);
+            if (dev_out[i]) cudaFree(dev_out[i]);
+            if (in_ready[i]) cudaEventDestroy(in_ready[i]);
+            if (step_done[i]) cudaEventDestroy(step_done[i]);
+            if (out_done[i]) cudaEventDestroy(out_done[i]);
+        }
+        for (int j = 0; j < OUT_CHUNKS; ++j)
+            if (out_chunk[j]) cudaEventDestroy(out_chunk[j]);
+        if (pin_in) cudaFreeHost(pin_in);
+        if (pin_out) cudaFreeHost(pin_out);
+        if (s_in) cudaStreamDestroy(s_in);
+        if (s_out) cudaStreamDestroy(s_out);
+        *this = HostStaging();
+    }
+
+    // One frame: in (in_bytes) -> step(dev frame, dev mask) on `st` -> out
+    // (out_bytes).  sync = 1: pageable caller buffers, returns with the mask
+    // in `out`; sync = 0: pinned caller buffers, returns after enqueueing.
+    template <typename Step>
+    int run(const uint8_t* in, uint8_t* out, int sync, cudaStream_t st, Step step) {
+        const int k = slot;
+        slot ^= 1;
+        // the slot's previous frame: its step read dev_in[k] and its
+        // download read dev_out[k]
+        if (used[k]) {
+            RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(s_in, step_done[k], 0));
+            RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(st, out_done[k], 0));
+        }
+        used[k] = true;
+        if (sync) {
+            // pin_in / pin_out are free: the previous sync call drained them,
+            // and async calls never touch them
+            const int64_t ch = ((in_bytes + IN_CHUNKS - 1) / IN_CHUNKS + 4095) / 4096 * 4096;  // >= 4096
+            for (int64_t off = 0; off < in_bytes; off += ch) {
+                const int64_t n = in_bytes - off < ch ? in_bytes - off : ch;
+                memcpy(pin_in + off, in + off, (size_t)n);
+                RGBDSEG_CUDA_TRY(cudaMemcpyAsync(dev_in[k] + off, pin_in + off, n,
+                                                 cudaMemcpyHostToDevice, s_in));
+            }
+        } else {
+            RGBDSEG_CUDA_TRY(cudaMemcpyAsync(dev_in[k], in, in_bytes, cudaMemcpyHostToDevice, s_in));
+        }
+        RGBDSEG_CUDA_TRY(cudaEventRecord(in_ready[k], s_in));
+        RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(st, in_ready[k], 0));
+        if (int rc = step(dev_in[k], dev_out[k], st)) return rc;
+        RGBDSEG_CUDA_TRY(cudaEventRecord(step_done[k], st));
+        RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(s_out, step_done[k], 0));
+        if (sync) {
+            const int64_t ch = ((out_bytes + OUT_CHUNKS - 1) / OUT_CHUNKS + 4095) / 4096 * 4096;  // >= 4096
+            int nch = 0;
+            for (int64_t off = 0; off < out_bytes; off += ch, ++nch) {
+                const int64_t n = out_bytes - off < ch ? out_bytes - off : ch;
+                RGBDSEG_CUDA_TRY(cudaMemcpyAsync(pin_out + off, dev_out[k] + off, n,
+                                                 cudaMemcpyDeviceToHost, s_out));
+                RGBDSEG_CUDA_TRY(cudaEventRecord(out_chunk[nch], s_out));
+            }
+            RGBDSEG_CUDA_TRY(cudaEventRecord(out_done[k], s_out));
+            nch = 0;
+            for (int64_t off = 0; off < out_bytes; off += ch, ++nch) {
+                const int64_t n = out_bytes - off < ch ? out_bytes - off : ch;
+                RGBDSEG_CUDA_TRY(cudaEventSynchronize(out_chunk[nch]));
+                memcpy(out + off, pin_out + off, (size_t)n);
+            }
+        } else {
+            RGBDSEG_CUDA_TRY(cudaMemcpyAsync(out, dev_out[k], out_bytes, cudaMemcpyDeviceToHost, s_out));
+            RGBDSEG_CUDA_TRY(cudaEventRecord(out_done[k], s_out));
+        }
+        return RGBDSEG_OK;
+    }
+
+    // Everything enqueued by run() has finished.
+    int drain() {
+        if (s_in) RGBDSEG_CUDA_TRY(cudaStreamSynchronize(s_in));
+        if (s_out) RGBDSEG_CUDA_TRY(cudaStreamSynchronize(s_out));
+        return RGBDSEG_OK;
+    }
+};
 
 // ------------------------------------------------------------- tracing --
 // NVTX range around every C-ABI step (SURVEY.md §5 "tracing"): what an

@@ -967,3 +967,88 @@ def test_mixed_input_kinds_stay_ordered(oracle_mod, algo):
         torch.cuda.synchronize()
         st = {k: v for k, v in eng.state_arrays().items()}
     _assert_state_equal(st, ref.state_arrays(), list(st))
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_submit_pipelined_sequence_matches_oracle(oracle_mod, algo):
+    # SegmentationEngine.submit(): frames from pinned host buffers enqueued
+    # back to back with no synchronisation in between (frame t+1's upload
+    # overlaps frame t's kernels and frame t-1's download, two device slots
+    # per handle), then one synchronize(): every mask equals the oracle's
+    # sequential run (engine.py:99-112 semantics), and so does the state.
+    import torch
+
+    w, h, n = 640, 480, 24
+    cfg = (PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=7, k_d=3))
+           if algo == "gmm" else
+           PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=6), seed=11))
+    frames = synth.sequence("S" if algo == "gmm" else "T", w, h, seed=5, frames=n)
+    pinned_in = [torch.from_numpy(f).pin_memory().numpy() for f in frames]
+    pinned_out = [torch.empty((h, w), dtype=torch.uint8).pin_memory().numpy() for _ in frames]
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    with _engine(cfg, w, h) as eng:
+        for f, m in zip(pinned_in, pinned_out):
+            eng.submit(f, m)
+        eng.synchronize()
+        for t, f in enumerate(frames):
+            np.testing.assert_array_equal(pinned_out[t], ref.process_frame(f), err_msg=f"frame {t}")
+        # the synchronous staged path continues the same state
+        for t in range(4):
+            f = synth.make_frame("S" if algo == "gmm" else "T", w, h, 5, n + t)
+            np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
+                                          err_msg=f"frame {n + t} (process_frame)")
+        st = {k: v for k, v in eng.state_arrays().items()}
+    _assert_state_equal(st, ref.state_arrays(), list(st))
+
+
+@pytest.mark.parametrize("k", [3, 7])
+def test_gmm_least_fit_near_ties_match_reference(oracle_mod, k):
+    # Unmatched pixels replace argmin_k w_k / sqrt(v_k) (gmm.py:326-337,
+    # first minimum wins).  K1 picks it from an FP32 estimate unless the
+    # runner-up is within 2^-16 of the minimum (or a value is out of range);
+    # these states put the exact FP64 keys at exact ties, 1-ulp and 1e-9 /
+    # 1e-6 / 1e-5 / 3e-5 / 1e-3 relative gaps in every slot order, plus +0
+    # weights and tiny / huge values, and check every replacement against
+    # the oracle.
+    rng = np.random.default_rng(17 + k)
+    w_, h_ = 64, 48
+    P = w_ * h_
+    cfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=k, k_d=3))
+    ref = oracle_mod.OracleEngine(cfg, w_, h_, workers=1)
+    ref.process_frame(synth.make_frame("T", w_, h_, 1, 0))
+    st = {key: v.copy() for key, v in ref.state_arrays().items()}
+    gaps = [0.0, 2.0 ** -52, 1e-9, 1e-6, 1e-5, 3e-5, 1e-3, 0.5]
+    wv = np.empty((P, k))
+    vv = np.empty((P, k))
+    for i in range(P):
+        base_f = rng.uniform(0.05, 0.3)
+        v = rng.uniform(1.0, 400.0, size=k)
+        f = base_f * (1.0 + rng.uniform(0.01, 1.0, size=k))  # well separated ...
+        a, b = rng.choice(k, size=2, replace=False)  # ... except a near-tied pair
+        g = gaps[i % len(gaps)]
+        f[a] = base_f
+        f[b] = base_f * (1.0 + g)
+        wv[i] = f * np.sqrt(v)
+        vv[i] = v
+        if i % 97 == 5:  # two +0 weights (ties at 0)
+            wv[i, a] = 0.0
+            wv[i, b] = 0.0
+        if i % 89 == 7:  # out of the FP32 estimate's range
+            wv[i, a] = 1e-20
+        if i % 83 == 11:
+            wv[i, b] = 1e20
+    st["rgb_w"] = wv.reshape(h_, w_, k)
+    st["rgb_var"] = vv.reshape(h_, w_, k)
+    st["rgb_mu"] = np.full((h_, w_, k, 3), 10.0)  # far from the frame below: no match
+    ref.state = {key: v.copy() for key, v in st.items()}
+    frame = np.zeros((h_, w_, 4), np.uint8)
+    frame[..., :3] = 240
+    frame[..., 3] = 0  # no depth: the RGB sub-model alone
+    with _engine(cfg, w_, h_) as eng:
+        eng.load_state(st)
+        np.testing.assert_array_equal(eng.process_frame(frame), ref.process_frame(frame))
+        got = {key: v for key, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), gu.GMM_KEYS)
+    # the replaced slot differs between the near-tied pair across pixels
+    replaced = np.argmax(ref.state_arrays()["rgb_mu"][..., 0].reshape(P, k) == 240.0, axis=1)
+    assert len(np.unique(replaced)) == k
