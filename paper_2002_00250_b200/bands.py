@@ -49,8 +49,20 @@ def band_bounds(height: int, parts: int):
     return [(int(edges[i]), int(edges[i + 1])) for i in range(parts)]
 
 
+def band_neighbours(height: int, world: int, rank: int):
+    """(above, below): the nearest ranks whose bands hold rows, or None at
+    the frame edge.  With more bands than rows (engine.py:48-50 gives empty
+    bands, tests/test_engine.py:120-127) an empty band is skipped: the row
+    right below band r's last row is the first row of the next non-empty
+    band."""
+    b = band_bounds(height, world)
+    above = next((r for r in range(rank - 1, -1, -1) if b[r][1] > b[r][0]), None)
+    below = next((r for r in range(rank + 1, world) if b[r][1] > b[r][0]), None)
+    return above, below
+
+
 def exchange_intent_halos(first_row, last_row, halo_above, halo_below, rank: int, world: int,
-                          group=None, wait: bool = True):
+                          group=None, wait: bool = True, peers=None):
     """One-row intent halo exchange between adjacent bands.
 
     Sends this band's first intent row to rank-1 (it becomes that band's
@@ -58,19 +70,23 @@ def exchange_intent_halos(first_row, last_row, halo_above, halo_below, rank: int
     rank-1's last row into `halo_above` and rank+1's first row into
     `halo_below`.  At the global top/bottom the halo is "no intent".
     Works with any torch.distributed backend (NCCL on GPUs, gloo on CPU).
+    peers: (above, below) ranks (default rank-1 / rank+1; band_neighbours
+    when some bands are empty), None at a frame edge.
     Returns the pending works when wait=False.
     """
     import torch.distributed as dist
 
+    above, below = peers if peers is not None else (rank - 1 if rank > 0 else None,
+                                                   rank + 1 if rank < world - 1 else None)
     ops = []
-    if rank > 0:
-        ops.append(dist.P2POp(dist.isend, first_row, rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, halo_above, rank - 1, group))
+    if above is not None:
+        ops.append(dist.P2POp(dist.isend, first_row, above, group))
+        ops.append(dist.P2POp(dist.irecv, halo_above, above, group))
     else:
         halo_above.fill_(NONE_BYTE)
-    if rank < world - 1:
-        ops.append(dist.P2POp(dist.isend, last_row, rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, halo_below, rank + 1, group))
+    if below is not None:
+        ops.append(dist.P2POp(dist.isend, last_row, below, group))
+        ops.append(dist.P2POp(dist.irecv, halo_below, below, group))
     else:
         halo_below.fill_(NONE_BYTE)
     works = dist.batch_isend_irecv(ops) if ops else []
@@ -83,14 +99,16 @@ def exchange_intent_halos(first_row, last_row, halo_above, halo_below, rank: int
 
 def neighbour_handles(mine: bytes, rank: int, world: int, group=None):
     """All-gather the bands' mailbox handles (any torch.distributed backend)
-    and return (above, below): the handles of rank-1 and rank+1, None at the
-    frame's top / bottom edge."""
+    and return (above, below): the handles of the nearest bands above and
+    below that hold rows (empty bands contribute b""), None at the frame's
+    top / bottom edge."""
     import torch.distributed as dist
 
     handles = [None] * world
     dist.all_gather_object(handles, mine, group=group)
-    return (handles[rank - 1] if rank > 0 else None,
-            handles[rank + 1] if rank < world - 1 else None)
+    above = next((handles[r] for r in range(rank - 1, -1, -1) if handles[r]), None)
+    below = next((handles[r] for r in range(rank + 1, world) if handles[r]), None)
+    return above, below
 
 
 class HaloLink:
@@ -189,18 +207,26 @@ class RowBandPbas:
         self.rank, self.world, self.group = rank, world, group
         self.transport = transport
         self.y0, self.y1 = band_bounds(height, world)[rank]
-        self.engine = SegmentationEngine(config, width, height, device, _band=(self.y0, self.y1))
         self.rows = self.y1 - self.y0
+        self.peers = band_neighbours(height, world, rank)
+        # more bands than rows: an empty band has no engine and steps as a
+        # no-op; its neighbours link past it (band_neighbours)
+        self.engine = (SegmentationEngine(config, width, height, device, _band=(self.y0, self.y1))
+                       if self.rows > 0 else None)
         self.width = width
         self._L = _native.lib()
         self.link = None
         if world > 1 and transport == "p2p":
             import torch.distributed as dist
 
-            self.link = HaloLink(self.engine)
-            self.link.connect(*neighbour_handles(self.link.export(), rank, world, group))
+            if self.engine is not None:
+                self.link = HaloLink(self.engine)
+            mine = self.link.export() if self.link is not None else b""
+            above, below = neighbour_handles(mine, rank, world, group)
+            if self.link is not None:
+                self.link.connect(above, below)
             dist.barrier(group)  # every mailbox mapped before the first push
-        elif world > 1:
+        elif world > 1 and self.engine is not None:
             import torch.distributed as dist
 
             if dist.get_backend(group) != "nccl":
@@ -215,6 +241,8 @@ class RowBandPbas:
     def step(self, band_frame, band_mask) -> None:
         """Segment this band of one frame (device tensors, (rows, W, 4) and
         (rows, W) uint8), exchanging the intent halos with the neighbours."""
+        if self.engine is None:  # empty band (more bands than rows)
+            return
         st = ctypes.c_void_p(torch_stream_handle(band_frame.device))
         fp, mp = ctypes.c_void_p(band_frame.data_ptr()), ctypes.c_void_p(band_mask.data_ptr())
         if self.world == 1 or self.transport == "p2p":
@@ -234,14 +262,14 @@ class RowBandPbas:
         _native.check(L.rgbdseg_pbas_copy_edges(h, ctypes.c_void_p(s0.data_ptr()),
                                                 ctypes.c_void_p(s1.data_ptr()), st), "copy_edges")
         works = exchange_intent_halos(s0, s1, self._recv[0], self._recv[1], self.rank,
-                                      self.world, self.group, wait=False)
+                                      self.world, self.group, wait=False, peers=self.peers)
         if rows > 2:  # interior rows overlap the exchange
             _native.check(L.rgbdseg_pbas_classify_rows(h, fp, mp, 1, rows - 1, st),
                           "classify interior")
         for w in works:
             w.wait()
-        above = ctypes.c_void_p(self._recv[0].data_ptr()) if self.rank > 0 else None
-        below = ctypes.c_void_p(self._recv[1].data_ptr()) if self.rank < self.world - 1 else None
+        above = ctypes.c_void_p(self._recv[0].data_ptr()) if self.peers[0] is not None else None
+        below = ctypes.c_void_p(self._recv[1].data_ptr()) if self.peers[1] is not None else None
         _native.check(L.rgbdseg_pbas_set_halos(h, above, below, st), "set_halos")
         _native.check(L.rgbdseg_pbas_apply(h, fp, st), "apply")
 
@@ -254,4 +282,5 @@ class RowBandPbas:
         if self.link is not None:
             self.link.close()
             self.link = None
-        self.engine.close()
+        if self.engine is not None:
+            self.engine.close()

@@ -24,6 +24,15 @@ Fixtures:
   frames.npz              frames.pack_frame(rgb, resample_depth(d16, W, H))
                           (frames.py:46-88): all 65536 depth values plus
                           up/down/odd mixed-resolution pairs
+  accept_c3.npz           acceptance criterion 3 (tests/test_acceptance.py:
+                          125-139): 500 noisy 64x64 frames (default_rng(99)),
+                          default GMM, workers=2 -- packed masks, per-frame
+                          weight-sum / variance extremes, sha256 of the
+                          final state
+  accept_c7.npz           acceptance criterion 7 (:200-233): the 160x120x200
+                          colour_camouflage scene, seed 42, GMM and PBAS,
+                          workers 1 -- packed masks, sha256 of every input
+                          frame and of the final state
 """
 
 from __future__ import annotations
@@ -193,8 +202,58 @@ def make_frames():
     _save("frames.npz", **out)
 
 
+def _sha(a) -> str:
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def make_accept_c3():
+    """Criterion 3 (tests/test_acceptance.py:125-139), the reference engine."""
+    rng = np.random.default_rng(99)
+    cfg = PipelineConfig(algorithm="gmm", mode="rgbd", workers=2)
+    masks, wsum_dev, var_min = [], [], []
+    with SegmentationEngine(cfg, 64, 64) as eng:
+        state = eng.state_arrays()
+        for _ in range(500):
+            frame = rng.integers(0, 256, size=(64, 64, 4), dtype=np.uint8)
+            frame[:, :, 3] = rng.integers(1, 256, size=(64, 64))  # always valid
+            masks.append(np.packbits(eng.process_frame(frame) > 0))
+            wsum_dev.append(max(float(np.abs(state[k].sum(axis=2) - 1.0).max())
+                                for k in ("rgb_w", "d_w")))
+            var_min.append(min(float(state[k].min()) for k in ("rgb_var", "d_var")))
+        st = {k: v.copy() for k, v in eng.state_arrays().items()}
+    _save("accept_c3.npz", masks=np.stack(masks), wsum_dev=np.array(wsum_dev),
+          var_min=np.array(var_min), state_keys=np.array(sorted(st)),
+          state_sha=np.array([_sha(st[k]) for k in sorted(st)]))
+
+
+def make_accept_c7():
+    """Criterion 7 (tests/test_acceptance.py:200-233): the reference's scene
+    frames (synth.rgb_at / depth16_at, what write_sequence stores as PNG,
+    lossless) packed by frames.pack_frame, through the reference engine."""
+    from rgbdseg import frames as ref_frames
+    from rgbdseg.synth import SynthSpec, depth16_at, rgb_at
+
+    spec = SynthSpec(scenario="colour_camouflage", width=160, height=120, frames=200,
+                     entry_frame=100)
+    frames = [ref_frames.pack_frame(rgb_at(spec, t), depth16_at(spec, t))
+              for t in range(spec.frames)]
+    out = {"frame_sha": np.array([_sha(f) for f in frames]),
+           "rgb_sha": np.array([_sha(rgb_at(spec, t)) for t in range(spec.frames)]),
+           "d16_sha": np.array([_sha(depth16_at(spec, t)) for t in range(spec.frames)])}
+    for algo in ("gmm", "pbas"):
+        cfg = PipelineConfig(algorithm=algo, mode="rgbd", seed=42, workers=1)
+        masks, st = _engine_run(cfg, frames)
+        out[f"{algo}_masks"] = np.stack([np.packbits(m > 0) for m in masks])
+        out[f"{algo}_state_keys"] = np.array(sorted(st))
+        out[f"{algo}_state_sha"] = np.array([_sha(st[k]) for k in sorted(st)])
+    _save("accept_c7.npz", **out)
+
+
 MAKERS = {"rng": make_rng, "gmm_equiv": make_gmm_equiv, "pbas_equiv": make_pbas_equiv,
-          "gmm_seq": make_gmm_seq, "pbas_seq": make_pbas_seq, "frames": make_frames}
+          "gmm_seq": make_gmm_seq, "pbas_seq": make_pbas_seq, "frames": make_frames,
+          "accept_c3": make_accept_c3, "accept_c7": make_accept_c7}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or MAKERS):

@@ -50,12 +50,12 @@ def _pull_apply(state, frame, codes_padded, y0, rows, use_depth):
         state["samples"][y0 + ly, lx, slots] = val[y0 + ly, lx]
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, H=H):
     import torch
     import torch.distributed as dist
 
     from oracle import oracle
-    from paper_2002_00250_b200.bands import exchange_intent_halos
+    from paper_2002_00250_b200.bands import band_neighbours, exchange_intent_halos
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -64,9 +64,13 @@ def _worker(rank, world, port, out_path):
     state = oracle.pbas_state(W, H, cfg.pbas)
     y0, y1 = band_bounds(H, world)[rank]
     rows = y1 - y0
+    peers = band_neighbours(H, world, rank)
     masks = []
     crossing = 0
     for f_idx, frame in enumerate(frames):
+        if rows == 0:  # more bands than rows: an empty band is harmless (test_engine.py:120-127)
+            masks.append(np.zeros((0, W), dtype=np.uint8))
+            continue
         mask = np.zeros((H, W), dtype=np.uint8)
         intents, emitters = oracle.pbas_band_emit(cfg, state, frame, f_idx, y0, y1, mask)
         masks.append(mask[y0:y1].copy())
@@ -79,7 +83,7 @@ def _worker(rank, world, port, out_path):
         first, last = torch.from_numpy(codes[0].copy()), torch.from_numpy(codes[-1].copy())
         above = torch.empty(W, dtype=torch.uint8)
         below = torch.empty(W, dtype=torch.uint8)
-        exchange_intent_halos(first, last, above, below, rank, world)
+        exchange_intent_halos(first, last, above, below, rank, world, peers=peers)
         padded = np.full((rows + 2, W + 2), NONE_BYTE, dtype=np.uint8)
         padded[0, 1:-1] = above.numpy()
         padded[1:-1, 1:-1] = codes
@@ -94,17 +98,19 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_row_band_halo_exchange_matches_single_process(oracle_mod, tmp_path, world):
+@pytest.mark.parametrize("world,h", [(2, H), (3, H), (5, 3)])
+def test_row_band_halo_exchange_matches_single_process(oracle_mod, tmp_path, world, h):
+    # (5, 3): more bands than rows -- two empty bands, their neighbours
+    # exchange halos past them (bands.band_neighbours)
     import torch.multiprocessing as mp
 
     out = tmp_path / "bands.npy"
-    mp.start_processes(_worker, args=(world, _free_port(), str(out)), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), str(out), h), nprocs=world,
                        start_method="spawn", join=True)
     parts = np.load(out, allow_pickle=True)
 
-    ref = oracle_mod.OracleEngine(_cfg(), W, H, workers=1)
-    frames = synth.sequence("T", W, H, seed=4, frames=NFRAMES)
+    ref = oracle_mod.OracleEngine(_cfg(), W, h, workers=1)
+    frames = synth.sequence("T", W, h, seed=4, frames=NFRAMES)
     ref_masks = np.stack([ref.process_frame(f) for f in frames])
     assert sum(int(p[4]) for p in parts) > 0  # intents really crossed band boundaries
     for y0, y1, own, masks, _ in parts:
@@ -150,3 +156,12 @@ def test_peer_link_handles_go_to_adjacent_bands(tmp_path, world):
     for r, (above, below) in enumerate(got):
         assert above == (bytes([r - 1]) * 64 if r > 0 else None)
         assert below == (bytes([r + 1]) * 64 if r < world - 1 else None)
+
+
+def test_band_neighbours_skip_empty_bands():
+    from paper_2002_00250_b200.bands import band_neighbours
+
+    # 3 rows over 5 bands: (0,0) (0,1) (1,1) (1,2) (2,3)
+    assert [band_neighbours(3, 5, r) for r in range(5)] == [
+        (None, 1), (None, 3), (1, 3), (1, 4), (3, None)]
+    assert [band_neighbours(10, 3, r) for r in range(3)] == [(None, 1), (0, 2), (1, None)]
