@@ -219,6 +219,38 @@ def _gen_ring(regime, w, h, seeds, ring, k_rgb=7):
     return np.stack(frames).reshape(len(seeds), ring, h, w, 4)
 
 
+# --------------------------------------------------------- bit equality ----
+def _fold_dev(t) -> int:
+    """Position-weighted 64-bit fold of a device tensor's bytes (wrapping
+    int64 arithmetic): equal bytes at equal positions <=> equal folds, up to
+    2^-64 collisions.  Used to prove a row-band / multi-rank run equals the
+    single-band one without moving the data."""
+    import torch
+
+    b = t.contiguous().view(torch.uint8).flatten()
+    pad = (-b.numel()) % 8
+    if pad:
+        b = torch.cat([b, torch.zeros(pad, dtype=torch.uint8, device=b.device)])
+    words = b.view(torch.int64)
+    idx = torch.arange(words.numel(), device=words.device, dtype=torch.int64) * 2 + 1
+    return int((words * idx).sum().item())
+
+
+def _fold_np(a) -> int:
+    b = np.ascontiguousarray(a).view(np.uint8).ravel()
+    pad = (-b.size) % 8
+    if pad:
+        b = np.concatenate([b, np.zeros(pad, np.uint8)])
+    words = b.view(np.uint64)
+    idx = np.arange(words.size, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    with np.errstate(over="ignore"):
+        return int((words * idx).sum(dtype=np.uint64))
+
+
+def _mix(acc: int, v: int) -> int:
+    return ((acc * 0x9E3779B97F4A7C15) ^ (v & 0xFFFFFFFFFFFFFFFF)) & 0xFFFFFFFFFFFFFFFF
+
+
 # --------------------------------------------------------- CPU baseline ----
 def _native_k2_mode(ms_engine) -> int:
     from paper_2002_00250_b200 import _native
@@ -570,6 +602,26 @@ def run_ours(args, rank, world, local_rank):
         gbs = balg * npix * S / (young["ms_per_step"] / 1e3) / 1e9
         young.update({"achieved_gbs": gbs, "roofline_frac": gbs / peak_y})
 
+    # ---- per-stream digests (untimed): a stream's result depends only on its
+    # global id (content seed, PBAS seed), never on how many GPUs share the
+    # job, so stream g's digest must be identical in the N = 1, 2, 4, 8 runs
+    digests = None
+    if not args.no_verify:
+        mine = {}
+        for i, g in enumerate(stream_ids):
+            acc = 0
+            for name, eng, _, _ in algos:
+                acc = _mix(acc, _fold_dev(masks[name][i]))
+                st_i = eng.engines[i].state_arrays()
+                acc = _mix(acc, _fold_np(st_i["rgb_w" if name == "gmm" else "samples"]))
+            mine[g] = f"{acc:016x}"
+        if world > 1:
+            allv = [None] * world
+            dist.all_gather_object(allv, mine)
+            digests = {k: v for d in allv for k, v in d.items()}
+        else:
+            digests = mine
+
     # ---- e2e through the public host-buffer API (rank-local, then max)
     e2e = None
     if not args.no_e2e:
@@ -632,6 +684,11 @@ def run_ours(args, rank, world, local_rank):
             "fg_fraction_last_step": float(counters[0].item()) / float(counters[1].item()),
             "model_age": age_info,
             "pbas_young": young,
+            "stream_digests": digests,
+            "stream_digest_check": ("per global stream id: 64-bit folds of its last GMM and PBAS "
+                                    "masks, GMM rgb_w and PBAS samples after the run; a stream's "
+                                    "digest must not depend on the GPU count"),
+            "ranks": world,
         }
         print(json.dumps(line), flush=True)
     for _, eng, _, _ in algos:
@@ -660,13 +717,16 @@ def run_config5(args, rank, world, local_rank):
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     t = 0
+    acc = 0  # fold of this band's mask, every untimed frame (bit-equality proof)
     for _ in range(2 * n):  # burn-in: warm-up fill + full dmin rings
         band.step(ring[t % 4], mask)
+        acc = _mix(acc, _fold_dev(mask))
         t += 1
     clocks = ClockSampler(int(os.environ.get("RGBDSEG_NVSMI_INDEX", local_rank)), _pci_bus_id(dev))
     clocks.start()  # sampling spans warm-up + timed region (both under full load)
     for _ in range(args.warmup):  # BASELINE config 5 is a 60-frame sequence: stay young
         band.step(ring[t % 4], mask)
+        acc = _mix(acc, _fold_dev(mask))
         t += 1
     torch.cuda.synchronize()
     if world > 1:
@@ -684,6 +744,43 @@ def run_config5(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     elapsed_ms = float(ms.item())
+    # ---- bit-equality proof (untimed): this band's mask folds over the
+    # untimed frames, its last mask and its final state, gathered on rank 0
+    # and compared with a one-band run of the same frames on rank 0's GPU
+    mine = [acc, _fold_dev(mask)]
+    if band.engine is not None:
+        stt = band.engine.state_arrays()
+        mine += [_fold_np(stt[k]) for k in sorted(stt)]
+    bit_equal = None
+    if world > 1 and not args.no_verify:
+        allv = [None] * world
+        dist.all_gather_object(allv, (y0, y1, mine))
+        if rank == 0:
+            from paper_2002_00250_b200.bands import band_bounds
+            from paper_2002_00250_b200.engine import SegmentationEngine
+
+            full = torch.from_numpy(_gen_ring("T", w, h, [0], 4)[0]).to(dev)
+            fm = torch.empty((h, w), dtype=torch.uint8, device=dev)
+            bounds = band_bounds(h, world)
+            accs = [0] * world
+            with SegmentationEngine(cfg, w, h, device=local_rank) as one:
+                for k in range(t):
+                    one.step_device(full[k % 4].data_ptr(), fm.data_ptr(),
+                                    torch.cuda.current_stream(dev).cuda_stream)
+                    if k < t - args.steps:
+                        accs = [_mix(a, _fold_dev(fm[b0:b1])) for a, (b0, b1) in zip(accs, bounds)]
+                ost = one.state_arrays()
+                ost = {k: ost[k] for k in sorted(ost)}
+                want = []
+                for r, (b0, b1) in enumerate(bounds):
+                    wv = [accs[r], _fold_dev(fm[b0:b1])]
+                    if b1 > b0:
+                        wv += [_fold_np(v[b0:b1]) for v in ost.values()]
+                    want.append((b0, b1, wv))
+            bit_equal = [tuple(x) for x in allv] == want
+            del full
+    elif world == 1:
+        bit_equal = True  # the single band is the reference layout itself
     peak, peak_kind = measured_peaks()
     band_px = (y1 - y0) * w
     achieved = B_ALG[("pbas", n)] * band_px * args.steps / (elapsed_ms / 1e3) / 1e9
@@ -712,6 +809,13 @@ def run_config5(args, rank, world, local_rank):
                               .rgbdseg_pbas_get_k2_mode(band.engine._h.ptr)) == 2 else "rows"},
             "gpu_launches": args.steps * (2 if world == 1 else 6),
             "clocks": clock_info,
+            "bit_equal_across_gpus": bit_equal,
+            "bit_equal_check": ("every band's mask on every untimed frame, its last mask and its "
+                                "final state (position-weighted 64-bit folds), gathered from "
+                                f"{world} rank(s) and compared with a one-band run of the same "
+                                f"{t} frames on rank 0" if world > 1 else "single band"),
+            "ranks": world,
+            "collective_backend": (dist.get_backend() if world > 1 else None),
         }
         print(json.dumps(line), flush=True)
     band.close()
@@ -902,6 +1006,8 @@ def main():
     ap.add_argument("--pbas-age", type=int, default=400,
                     help="PBAS burn-in frames before timing (400: T at t_lower, steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="skip the untimed cross-rank bit-equality proof")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="config5 row-band intent-halo transport")

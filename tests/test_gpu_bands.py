@@ -40,7 +40,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, W=W, H=H):
     import torch
     import torch.distributed as dist
 
@@ -75,15 +75,17 @@ def _reference(oracle_mod, frames, w, h, cfg):
     return ref, np.stack([ref.process_frame(f) for f in frames])
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_row_band_pbas_ranks_ipc_match_single_engine(oracle_mod, tmp_path, world):
+@pytest.mark.parametrize("world,w,h", [(2, W, H), (3, W, H), (4, 7680, 48)])
+def test_row_band_pbas_ranks_ipc_match_single_engine(oracle_mod, tmp_path, world, w, h):
+    # (4, 7680, 48): four ranks at the 8K width of BASELINE config 5, so the
+    # mailboxes carry production-size halo rows (7680 codes per boundary)
     import torch.multiprocessing as mp
 
     out = tmp_path / "bands.npy"
-    mp.start_processes(_worker, args=(world, _port(), str(out)), nprocs=world,
+    mp.start_processes(_worker, args=(world, _port(), str(out), w, h), nprocs=world,
                        start_method="spawn", join=True)
     parts = np.load(out, allow_pickle=True)
-    ref, ref_masks = _reference(oracle_mod, synth.sequence("T", W, H, seed=8, frames=NF), W, H,
+    ref, ref_masks = _reference(oracle_mod, synth.sequence("T", w, h, seed=8, frames=NF), w, h,
                                 _cfg())
     for y0, y1, masks, state in parts:
         np.testing.assert_array_equal(masks, ref_masks[:, y0:y1], err_msg=f"rows {y0}:{y1}")
