@@ -259,7 +259,8 @@ def _native_k2_mode(ms_engine) -> int:
 
 
 def _k2_name(ms_engine) -> str:
-    return "strips" if _native_k2_mode(ms_engine) == 2 else "rows"
+    return {1: "rows", 2: "strips", 3: "fused K2+K3 (one cooperative launch)"}.get(
+        _native_k2_mode(ms_engine), "?")
 
 
 def _cpu_model() -> str:
@@ -393,6 +394,13 @@ def run_ours(args, rank, world, local_rank):
         pcfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=pbas_n),
                               pbas_gradient=PbasGradient() if args.pbas_gradient else None)
         p = MultiStreamEngine(pcfg, w, h, S, device=local_rank, seeds=[s + 1 for s in stream_ids])
+        if args.k2_mode != "auto":  # pin the K2 variant (evidence runs; results are identical)
+            from paper_2002_00250_b200 import _native
+
+            for e in p.engines:
+                _native.check(_native.lib().rgbdseg_pbas_set_k2_mode(
+                    e._h.ptr, {"rows": 1, "strips": 2, "fused": 3, "unfused": 4}[args.k2_mode]),
+                    "set_k2_mode")
         ring_t = torch.from_numpy(_gen_ring("T", w, h, stream_ids, 8)).to(dev)
         algos.append(("pbas", p, ring_t,
                       B_ALG.get(("pbas_grad" if args.pbas_gradient else "pbas", pbas_n))))
@@ -1003,6 +1011,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--e2e-input", choices=["T", "S"], default="T",
                     help="camera frames of the shared-upload e2e leg (regime T or S)")
+    ap.add_argument("--k2-mode", choices=["auto", "rows", "strips", "fused", "unfused"], default="auto",
+                    help="pin PBAS's K2 variant (default: chosen per frame by the update rate)")
     ap.add_argument("--pbas-age", type=int, default=400,
                     help="PBAS burn-in frames before timing (400: T at t_lower, steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -245,11 +245,16 @@ void rgbdseg_halo_link_destroy(rgbdseg_halo_link* l);
  * RGBDSEG_PBAS_GRAD_PREV. */
 int rgbdseg_pbas_set_gradient(rgbdseg_pbas* h, int32_t enable, double alpha, double mean_init);
 /* K2 variant (performance only; every variant gives the same result):
- * 0 auto (default) -- the row kernel while few pixels emit neighbour updates,
- * the 32x8 tile kernel (in-tile updates applied inside K2) once many do, chosen
- * from the update count K3 posts each frame; 1 always rows; 2 always tiles
- * (tiles need a single-band handle with width % 32 == 0).  get returns the
- * variant the next step will use (1 rows, 2 tiles). */
+ * 0 auto (default) -- small frames (a whole single-band batch whose grid
+ * fits on the GPU at once) run K2 + K3 as ONE cooperative launch; larger ones
+ * run the row kernel while few pixels emit neighbour updates and the warp-strip
+ * kernel (in-strip updates applied inside K2) once many do, chosen from the
+ * update count K3 posts each frame; 1 always rows; 2 always strips (a
+ * single-band handle with width % 32 == 0); 3 fused whenever the step is
+ * eligible, else auto; 4 auto without the fused launch (rows / strips by
+ * the update rate).  get returns the variant of the
+ * latest step in auto mode when it ran fused (3), else the one the next step
+ * will use (1 rows, 2 strips).  Results are identical in every variant. */
 int rgbdseg_pbas_set_k2_mode(rgbdseg_pbas* h, int32_t mode);
 int32_t rgbdseg_pbas_get_k2_mode(const rgbdseg_pbas* h);
 int rgbdseg_pbas_step_batch(rgbdseg_pbas* const* hs, int32_t count,

@@ -69,36 +69,49 @@ def test_config3_720p_1000_frames_gmm_and_pbas_vs_oracle(oracle_mod):
     ref_g = oracle_mod.OracleEngine(gcfg, w, h, workers=threads)
     ref_p = oracle_mod.OracleEngine(pcfg, w, h, workers=threads)
     modes = []
+    # PBAS twice: auto (a single 720p stream runs K2 + K3 fused in one
+    # cooperative launch) and the auto row -> strip switch of bigger launches
+    # (fused disabled: rows while young, strips once T has decayed)
     with SegmentationEngine(gcfg, w, h, device=0) as eg, \
-            SegmentationEngine(pcfg, w, h, device=0) as ep:
+            SegmentationEngine(pcfg, w, h, device=0) as ep, \
+            SegmentationEngine(pcfg, w, h, device=0) as es:
         L = ep._h.L
+        assert L.rgbdseg_pbas_set_k2_mode(es._h.ptr, 4) == 0  # auto without the fused launch
         for t, f in enumerate(frames_ahead("T", w, h, seed=0, n=n)):
             mg = eg.process_frame(f)
             mp = ep.process_frame(f)
-            modes.append(int(L.rgbdseg_pbas_get_k2_mode(ep._h.ptr)))
+            ms = es.process_frame(f)
+            modes.append((int(L.rgbdseg_pbas_get_k2_mode(ep._h.ptr)),
+                          int(L.rgbdseg_pbas_get_k2_mode(es._h.ptr))))
             rg = ref_g.process_frame(f)
             rp = ref_p.process_frame(f)
             dg = int(np.count_nonzero(mg != rg))
             assert dg == 0, f"GMM frame {t}: {dg} mask pixels differ"
             np.testing.assert_array_equal(mp, rp, err_msg=f"PBAS frame {t}")
+            np.testing.assert_array_equal(ms, rp, err_msg=f"PBAS (rows/strips) frame {t}")
             if t + 1 in checkpoints:
                 _assert_state_equal(eg.state_arrays(), ref_g.state_arrays(), gu.GMM_KEYS,
                                     f"GMM after {t + 1} frames")
                 _assert_state_equal(ep.state_arrays(), ref_p.state_arrays(), gu.PBAS_KEYS,
                                     f"PBAS after {t + 1} frames")
+                _assert_state_equal(es.state_arrays(), ref_p.state_arrays(), gu.PBAS_KEYS,
+                                    f"PBAS (rows/strips) after {t + 1} frames")
     t_final = ref_p.state_arrays()["t"]
     at_lower = float(np.mean(t_final == pcfg.pbas.t_lower))
     tmed = float(np.median(t_final))
     # oracle run of this sequence: 0 % of the pixels at t_lower after 500
     # frames, 36 % after 600, 46 % after 1000 (T median 2.78)
     assert at_lower >= 0.4, f"only {at_lower:.3f} of the pixels reached t_lower"
-    # the production auto switch ran the tile K2 for the aged model ...
-    assert 2 in modes, "the auto K2 switch never chose the tile variant"
-    first_tile = modes.index(2)
-    assert modes[-1] == 2, "K2 is not on the tile variant at T = t_lower"
+    fused = [a for a, _ in modes]
+    assert set(fused[20:]) == {3}, "a single 720p stream should run fused"
+    sw = [b for _, b in modes]
+    # the rows -> strips switch of unfused launches ran for the aged model ...
+    assert 2 in sw, "the auto K2 switch never chose the strip variant"
+    first_tile = sw.index(2)
+    assert sw[-1] == 2, "K2 is not on the strip variant at T = t_lower"
     # ... and the row kernel while the model was young
-    assert modes[21] == 1
-    print(f"config 3: tile K2 from frame {first_tile}; T median at 1000 = {tmed}, "
+    assert sw[21] == 1
+    print(f"config 3: strip K2 from frame {first_tile}; T median at 1000 = {tmed}, "
           f"{at_lower:.3f} at t_lower")
 
 

@@ -767,13 +767,14 @@ def test_pbas_load_state_rejects_positions_outside_the_ring():
         eng.load_state({"len_d": ok})
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_pbas_k2_variants_and_auto_switch(oracle_mod, mode):
-    # K2 runs as the row kernel or as the 32x8 tile kernel that applies
-    # in-tile neighbour updates itself; auto mode switches on the update
-    # rate K3 posts.  A fast T decay (t_dec) drives the rate from ~1/18 to
-    # 1/2 within the sequence, so auto mode must cross over -- every frame
-    # bit-exact with the reference in every mode.
+    # K2 runs as the row kernel, as the warp-strip kernel that applies
+    # in-strip neighbour updates itself, or -- small frames, auto / pinned
+    # 3 -- fused with K3 in one cooperative launch.  A fast T decay (t_dec)
+    # drives the update rate from ~1/18 to 1/2 within the sequence -- every
+    # frame bit-exact with the reference in every mode.  (The auto row ->
+    # strip crossover of frames too big to fuse: the 1080p test below.)
     from paper_2002_00250_b200 import _native
 
     w, h, n = 96, 40, 6
@@ -790,8 +791,34 @@ def test_pbas_k2_variants_and_auto_switch(oracle_mod, mode):
             np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
                                           err_msg=f"frame {t}")
         got = {k: v.copy() for k, v in eng.state_arrays().items()}
+        last = int(L.rgbdseg_pbas_get_k2_mode(eng._h.ptr))
     _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
-    assert seen == ({1, 2} if mode == 0 else {mode})
+    assert seen - {1} == ({3} if mode in (0, 3) else {mode}) - {1}  # first get: before any step
+    assert last == (3 if mode in (0, 3) else mode)
+
+
+def test_pbas_auto_switch_rows_to_strips_1080p(oracle_mod):
+    # A frame too big for the fused cooperative launch (> 8 pixels per
+    # resident thread): auto mode runs the row kernel while few pixels emit
+    # neighbour updates and switches to strips once many do (T decays fast
+    # here); bit-exact with the reference every frame.
+    from paper_2002_00250_b200 import _native
+
+    w, h, n = 1920, 1080, 6
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", seed=8,
+                         pbas=PbasParams(n=n, t_dec=1.0, t_lower=2.0))
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    L = _native.lib()
+    modes = []
+    with _engine(cfg, w, h) as eng:
+        for t in range(40):
+            f = synth.make_frame("T", w, h, 13, t)
+            np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
+                                          err_msg=f"frame {t}")
+            modes.append(int(L.rgbdseg_pbas_get_k2_mode(eng._h.ptr)))
+        got = {k: v.copy() for k, v in eng.state_arrays().items()}
+    _assert_state_equal(got, ref.state_arrays(), gu.PBAS_KEYS)
+    assert modes[n] == 1 and modes[-1] == 2 and 3 not in modes, modes
 
 
 @pytest.mark.parametrize("n,mm,mode", [(40, 2, "rgbd"), (7, 3, "rgbd"), (20, 1, "rgb_only"),
