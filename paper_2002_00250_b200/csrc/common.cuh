@@ -4,9 +4,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <utility>
 
@@ -117,8 +121,93 @@ inline int order_after(cudaStream_t last, cudaStream_t st, cudaEvent_t ev) {
 //     buffers, ~19 GB/s) and no hidden synchronisation;
 //   * async: the caller's buffers (pinned, alive until sync) are DMA'd
 //     directly.
+// Two helper threads that stage a caller's pageable frame into page-locked
+// memory chunk by chunk (each copies half of every chunk), so the host copy
+// runs at two threads' bandwidth and overlaps the calling thread's CUDA API
+// calls (the per-chunk DMA / kernel / download enqueues).  Idle helpers spin
+// briefly after a frame (back-to-back frames find them awake), then sleep on
+// a condition variable.
+struct CopyCrew {
+    static constexpr int NT = 2;
+    std::thread th[NT];
+    std::mutex mu;
+    std::condition_variable cv;
+    std::atomic<uint64_t> gen{0};
+    std::atomic<bool> quit{false};
+    const uint8_t* src = nullptr;
+    uint8_t* dst = nullptr;
+    int64_t chunk = 0, total = 0;
+    int nchunks = 0;
+    std::atomic<uint64_t> done[NT];  // (job generation << 32) | chunks copied
+    bool started = false;
+
+    void start() {
+        if (started) return;
+        for (int t = 0; t < NT; ++t) done[t].store(0);
+        for (int t = 0; t < NT; ++t) th[t] = std::thread([this, t] { worker(t); });
+        started = true;
+    }
+    void stop() {
+        if (!started) return;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            quit.store(true);
+        }
+        cv.notify_all();
+        for (int t = 0; t < NT; ++t) th[t].join();
+        started = false;
+    }
+    void worker(int t) {
+        uint64_t seen = 0;
+        for (;;) {
+            for (int spin = 0; spin < 200000 && gen.load(std::memory_order_acquire) == seen &&
+                               !quit.load(std::memory_order_relaxed);
+                 ++spin) {
+            }
+            if (gen.load(std::memory_order_acquire) == seen) {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return gen.load(std::memory_order_acquire) != seen || quit.load(); });
+            }
+            if (quit.load()) return;
+            seen = gen.load(std::memory_order_acquire);
+            const uint64_t tag = seen << 32;
+            for (int c = 0; c < nchunks; ++c) {
+                const int64_t off = c * chunk, n = total - off < chunk ? total - off : chunk;
+                const int64_t half = (n / NT + 63) / 64 * 64;
+                const int64_t o = off + t * half;
+                const int64_t m = o >= off + n ? 0 : (off + n - o < half || t == NT - 1 ? off + n - o : half);
+                if (m > 0) memcpy(dst + o, src + o, (size_t)m);
+                done[t].store(tag | (uint64_t)(c + 1), std::memory_order_release);
+            }
+        }
+    }
+    // Stage src[0, total) into dst in `chunk`-byte chunks; returns at once.
+    void post(const uint8_t* s, uint8_t* d, int64_t ch, int64_t n) {
+        src = s;
+        dst = d;
+        chunk = ch;
+        total = n;
+        nchunks = (int)((n + ch - 1) / ch);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            gen.fetch_add(1, std::memory_order_release);
+        }
+        cv.notify_all();
+    }
+    // Chunk c of the latest post() is staged (each helper finished its part).
+    void wait_chunk(int c) {
+        const uint64_t want = (gen.load(std::memory_order_relaxed) << 32) | (uint64_t)(c + 1);
+        for (int t = 0; t < NT; ++t)
+            while (done[t].load(std::memory_order_acquire) < want) {
+            }
+    }
+    void wait_all() {
+        if (nchunks > 0) wait_chunk(nchunks - 1);
+    }
+};
+
 struct HostStaging {
-    static constexpr int IN_CHUNKS = 8, OUT_CHUNKS = 4;
+    static constexpr int IN_CHUNKS = 8, OUT_CHUNKS = 4, ROW_CHUNKS = 8;
     int64_t in_bytes = 0, out_bytes = 0;
     uint8_t* pin_in = nullptr;
     uint8_t* pin_out = nullptr;
@@ -126,8 +215,41 @@ struct HostStaging {
     uint8_t* dev_out[2] = {nullptr, nullptr};
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t in_ready[2] = {}, step_done[2] = {}, out_done[2] = {}, out_chunk[OUT_CHUNKS] = {};
+    cudaEvent_t chunk_in[ROW_CHUNKS + 1] = {}, chunk_step[ROW_CHUNKS + 1] = {},
+                chunk_out[ROW_CHUNKS + 1] = {};
     bool used[2] = {false, false};
     int slot = 0;
+    // The process-wide helper crew (one pair of threads for every handle, so
+    // alternating GMM / PBAS calls keep it awake), held for one call at a
+    // time; a concurrent caller copies on its own thread instead.
+    CopyCrew* crew = nullptr;
+    std::unique_lock<std::mutex> crew_hold;
+    static constexpr int64_t CREW_MIN_BYTES = 1 << 20;   // smaller frames copy on the caller
+    static constexpr int64_t ROWS_MIN_BYTES = 4 << 20;   // row-chunked device work from here up
+
+    static std::mutex& crew_mutex() {
+        static std::mutex m;
+        return m;
+    }
+    static CopyCrew* shared_crew() {
+        static CopyCrew* c = [] {
+            CopyCrew* k = new (std::nothrow) CopyCrew();
+            if (k) k->start();  // never stopped: lives for the process
+            return k;
+        }();
+        return c;
+    }
+    bool ensure_crew() {
+        crew_hold = std::unique_lock<std::mutex>(crew_mutex(), std::try_to_lock);
+        crew = crew_hold.owns_lock() ? shared_crew() : nullptr;
+        if (!crew && crew_hold.owns_lock()) crew_hold.unlock();
+        return crew != nullptr;
+    }
+    void drop_crew() {
+        if (crew) crew->wait_all();  // (error paths) nothing may still write pin_in
+        crew = nullptr;
+        if (crew_hold.owns_lock()) crew_hold.unlock();
+    }
 
     int ensure(int64_t ib, int64_t ob) {
         if (pin_in) return RGBDSEG_OK;
@@ -144,12 +266,18 @@ struct HostStaging {
         }
         for (int j = 0; j < OUT_CHUNKS; ++j)
             RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&out_chunk[j], cudaEventDisableTiming));
+        for (int j = 0; j <= ROW_CHUNKS; ++j) {
+            RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&chunk_in[j], cudaEventDisableTiming));
+            RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&chunk_step[j], cudaEventDisableTiming));
+            RGBDSEG_CUDA_TRY(cudaEventCreateWithFlags(&chunk_out[j], cudaEventDisableTiming));
+        }
         RGBDSEG_CUDA_TRY(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
         RGBDSEG_CUDA_TRY(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
         return RGBDSEG_OK;
     }
 
     void release() {
+        drop_crew();
         if (s_in) cudaStreamSynchronize(s_in);
         if (s_out) cudaStreamSynchronize(s_out);
         for (int i = 0; i < 2; ++i) {
@@ -161,6 +289,11 @@ struct HostStaging {
         }
         for (int j = 0; j < OUT_CHUNKS; ++j)
             if (out_chunk[j]) cudaEventDestroy(out_chunk[j]);
+        for (int j = 0; j <= ROW_CHUNKS; ++j) {
+            if (chunk_in[j]) cudaEventDestroy(chunk_in[j]);
+            if (chunk_step[j]) cudaEventDestroy(chunk_step[j]);
+            if (chunk_out[j]) cudaEventDestroy(chunk_out[j]);
+        }
         if (pin_in) cudaFreeHost(pin_in);
         if (pin_out) cudaFreeHost(pin_out);
         if (s_in) cudaStreamDestroy(s_in);
@@ -186,12 +319,19 @@ struct HostStaging {
             // pin_in / pin_out are free: the previous sync call drained them,
             // and async calls never touch them
             const int64_t ch = ((in_bytes + IN_CHUNKS - 1) / IN_CHUNKS + 4095) / 4096 * 4096;  // >= 4096
-            for (int64_t off = 0; off < in_bytes; off += ch) {
+            const bool helpers = in_bytes >= CREW_MIN_BYTES && ensure_crew();
+            if (helpers) crew->post(in, pin_in, ch, in_bytes);
+            int c = 0;
+            for (int64_t off = 0; off < in_bytes; off += ch, ++c) {
                 const int64_t n = in_bytes - off < ch ? in_bytes - off : ch;
-                memcpy(pin_in + off, in + off, (size_t)n);
+                if (helpers)
+                    crew->wait_chunk(c);
+                else
+                    memcpy(pin_in + off, in + off, (size_t)n);
                 RGBDSEG_CUDA_TRY(cudaMemcpyAsync(dev_in[k] + off, pin_in + off, n,
                                                  cudaMemcpyHostToDevice, s_in));
             }
+            if (helpers) drop_crew();
         } else {
             RGBDSEG_CUDA_TRY(cudaMemcpyAsync(dev_in[k], in, in_bytes, cudaMemcpyHostToDevice, s_in));
         }
@@ -221,6 +361,64 @@ struct HostStaging {
             RGBDSEG_CUDA_TRY(cudaEventRecord(out_done[k], s_out));
         }
         return RGBDSEG_OK;
+    }
+
+    // The synchronous path with the device work split in row chunks too:
+    // chunk i is staged, uploaded, segmented (rows_step on rows [r0, r1))
+    // and its mask rows downloaded while the calling thread stages chunk
+    // i+1, so the kernels and both DMAs hide under the host copy; finish()
+    // runs once after the last chunk (PBAS: the neighbour-update phase).
+    // Chunks hold a multiple of `align` rows (PBAS row launches start on
+    // 32-pixel boundaries).
+    template <typename RowsStep, typename Finish>
+    int run_rows(const uint8_t* in, uint8_t* out, cudaStream_t st, int64_t rows, int64_t in_row,
+                 int64_t out_row, int64_t align, RowsStep rows_step, Finish finish) {
+        const int k = slot;
+        slot ^= 1;
+        if (used[k]) {
+            RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(s_in, step_done[k], 0));
+            RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(st, out_done[k], 0));
+        }
+        used[k] = true;
+        int64_t ch = (rows + ROW_CHUNKS - 1) / ROW_CHUNKS;
+        ch = (ch + align - 1) / align * align;
+        int n = 0, taken = 0;  // chunks enqueued / masks copied out
+        auto take = [&](int j) {
+            const int64_t r0 = j * ch, r1 = r0 + ch < rows ? r0 + ch : rows;
+            memcpy(out + r0 * out_row, pin_out + r0 * out_row, (size_t)((r1 - r0) * out_row));
+        };
+        const bool helpers = ensure_crew();
+        if (helpers) crew->post(in, pin_in, ch * in_row, rows * in_row);
+        for (int64_t r0 = 0; r0 < rows; r0 += ch, ++n) {
+            // masks of finished chunks leave while later chunks still upload
+            while (taken < n && cudaEventQuery(chunk_out[taken]) == cudaSuccess) take(taken++);
+            const int64_t r1 = r0 + ch < rows ? r0 + ch : rows;
+            const int64_t ib = r0 * in_row, in_n = (r1 - r0) * in_row;
+            if (helpers)
+                crew->wait_chunk(n);
+            else
+                memcpy(pin_in + ib, in + ib, (size_t)in_n);
+            RGBDSEG_CUDA_TRY(cudaMemcpyAsync(dev_in[k] + ib, pin_in + ib, in_n, cudaMemcpyHostToDevice,
+                                             s_in));
+            RGBDSEG_CUDA_TRY(cudaEventRecord(chunk_in[n], s_in));
+            RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(st, chunk_in[n], 0));
+            if (int rc = rows_step(dev_in[k], dev_out[k], r0, r1, st)) return rc;
+            RGBDSEG_CUDA_TRY(cudaEventRecord(chunk_step[n], st));
+            RGBDSEG_CUDA_TRY(cudaStreamWaitEvent(s_out, chunk_step[n], 0));
+            const int64_t ob = r0 * out_row, out_n = (r1 - r0) * out_row;
+            RGBDSEG_CUDA_TRY(cudaMemcpyAsync(pin_out + ob, dev_out[k] + ob, out_n,
+                                             cudaMemcpyDeviceToHost, s_out));
+            RGBDSEG_CUDA_TRY(cudaEventRecord(chunk_out[n], s_out));
+        }
+        if (helpers) drop_crew();
+        if (int rc = finish(dev_in[k], dev_out[k], st)) return rc;
+        RGBDSEG_CUDA_TRY(cudaEventRecord(step_done[k], st));
+        RGBDSEG_CUDA_TRY(cudaEventRecord(out_done[k], s_out));
+        for (; taken < n; ++taken) {
+            RGBDSEG_CUDA_TRY(cudaEventSynchronize(chunk_out[taken]));
+            take(taken);
+        }
+        return RGBDSEG_OK;  // finish() may still run: later steps are stream-ordered
     }
 
     // Everything enqueued by run() has finished.
