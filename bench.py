@@ -452,19 +452,33 @@ def run_ours(args, rank, world, local_rank):
     young = None
     yw = (2 * pbas_n, 2 * pbas_n + 50) if pbas_n else None
     ev_y = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+    young_pairs = []  # small configs: every young frame timed alone after an L2 flush
     for t in range(burn):
-        if yw and "pbas" in streams and burn_of["pbas"] >= yw[1] and t in yw:
+        in_young = bool(yw and "pbas" in streams and burn_of["pbas"] >= yw[1])
+        if in_young and flush_buf is None and t in yw:
             ev_y[yw.index(t)].record(streams["pbas"])
-            if t == yw[1]:
-                torch.cuda.synchronize()
-                pe = next(a[1] for a in algos if a[0] == "pbas")
-                tt = pe.engines[0].state_arrays()["t"]
-                ms_y = ev_y[0].elapsed_time(ev_y[1]) / (yw[1] - yw[0])
-                young = {"frames": list(yw), "pbas_T_median": float(np.median(tt)),
-                         "ms_per_step": ms_y, "k2_variant": _k2_name(pe)}
+        if in_young and t == yw[1]:
+            torch.cuda.synchronize()
+            pe = next(a[1] for a in algos if a[0] == "pbas")
+            tt = pe.engines[0].state_arrays()["t"]
+            ms_y = (ev_y[0].elapsed_time(ev_y[1]) / (yw[1] - yw[0]) if flush_buf is None else
+                    statistics.mean(a.elapsed_time(b) for a, b in young_pairs))
+            young = {"frames": list(yw), "pbas_T_median": float(np.median(tt)),
+                     "ms_per_step": ms_y, "k2_variant": _k2_name(pe),
+                     "l2": "inputs larger than L2" if flush_buf is None else "L2 flushed per frame"}
+        timed_young = in_young and flush_buf is not None and yw[0] <= t < yw[1]
         for name, eng, ring, _ in algos:
             if t < burn_of[name]:
-                launch(name, eng, ring, t)
+                if timed_young and name == "pbas":
+                    with torch.cuda.stream(streams[name]):
+                        flush_l2(t)
+                    pair = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    pair[0].record(streams[name])
+                    launch(name, eng, ring, t)
+                    pair[1].record(streams[name])
+                    young_pairs.append(pair)
+                else:
+                    launch(name, eng, ring, t)
     torch.cuda.synchronize()
     t_frame_by = dict(burn_of)
 
