@@ -915,7 +915,7 @@ def run_e2e(args, algos, S, w, h, dev, world):
     ev1.record(first)
     torch.cuda.synchronize()
     dev_ms = ev0.elapsed_time(ev1) / 30
-    pipe = MultiCameraPipeline({}, w, h, S, device=dev.index, engines=engines)
+    pipe = MultiCameraPipeline({}, w, h, S, device=dev.index, engines=engines, depth=args.e2e_depth)
     pinned = torch.empty((R, S, h, w, 4), dtype=torch.uint8, pin_memory=True)
     pinned.copy_(src.transpose(0, 1))  # (R, S, H, W, 4): one batch per step
     host_out = [{name: torch.empty((S, h, w), dtype=torch.uint8, pin_memory=True) for name in engines}
@@ -1023,6 +1023,8 @@ def main():
     ap.add_argument("--stream-priority", type=int, default=0,
                     help="PBAS stream priority boost over GMM (0 = equal)")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--e2e-depth", type=int, default=3,
+                    help="device frame slots of the shared-upload e2e pipeline")
     ap.add_argument("--e2e-input", choices=["T", "S"], default="T",
                     help="camera frames of the shared-upload e2e leg (regime T or S)")
     ap.add_argument("--k2-mode", choices=["auto", "rows", "strips", "fused", "unfused"], default="auto",

@@ -12,7 +12,8 @@ every configured algorithm; masks come back to host memory):
                    streams (MultiStreamEngine); GMM (HBM-bound) and PBAS run
                    concurrently
   copy-out stream  device masks -> pinned host buffers
-`depth` device slots let frame t+1 upload while frame t computes and frame
+`depth` device slots (default 3: 95 % of the device-resident rate at 8 x 1080p vs 87 % with
+2, `profiles/r02/host_path/e2e_depth.txt`) let frame t+1 upload while frame t computes and frame
 t-1's masks download.  All ordering is by CUDA events; `synchronize()`
 waits for everything submitted.
 """
@@ -25,7 +26,7 @@ from .errors import DimensionError
 
 class MultiCameraPipeline:
     def __init__(self, configs: dict, width: int, height: int, n_streams: int,
-                 device: int | None = None, seeds=None, depth: int = 2, engines: dict = None):
+                 device: int | None = None, seeds=None, depth: int = 3, engines: dict = None):
         """configs: {name: PipelineConfig}; or pass already-built
         MultiStreamEngines as `engines` ({name: engine}) to reuse their state."""
         import torch
