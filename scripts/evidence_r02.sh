@@ -17,7 +17,10 @@ if [ -z "$SKIP_NCU" ]; then
     --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-verify \
     > gpurun_out/launches.log 2>&1
   # GMM: 8 burn-in + solo; PBAS: strips from ~frame 150 of the 400-frame ageing, K3 list at steady state
-  for ks in gmm_step:12 pbas_classify_strip:200 pbas_apply_list:350; do
+  # the strip K2 at T = t_lower from the pinned-variant micro (frame ~450)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:pbas_classify_strip -s 430 -c 1 \
+    -o gpurun_out/full_pbas_classify_strip python scripts/micro/pbas_t2_time.py 2 > gpurun_out/full_strip.log 2>&1
+  for ks in gmm_step:12 pbas_apply_list:350; do
     k=${ks%%:*}; skip=${ks##*:}
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
       -o gpurun_out/full_$k python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-verify \
