@@ -1079,3 +1079,32 @@ def test_gmm_least_fit_near_ties_match_reference(oracle_mod, k):
     # the replaced slot differs between the near-tied pair across pixels
     replaced = np.argmax(ref.state_arrays()["rgb_mu"][..., 0].reshape(P, k) == 240.0, axis=1)
     assert len(np.unique(replaced)) == k
+
+
+@pytest.mark.parametrize("algo", ["gmm", "pbas"])
+def test_staged_host_path_row_chunks_odd_size(oracle_mod, algo):
+    # process_frame(numpy) on a frame >= 4 MB runs the row-chunked staged
+    # path (csrc/common.cuh HostStaging::run_rows): chunk i segments while
+    # chunk i+1 is staged by the helper threads.  An odd width makes the PBAS
+    # chunks align to 32 rows (list-mode row launches start on 32-pixel
+    # boundaries) and leaves a ragged last chunk; masks and state must equal
+    # the oracle, and a numpy frame mixed with a CUDA-tensor frame stays ordered.
+    import torch
+
+    w, h, n = 1283, 833, 14
+    assert 4 * w * h >= 4 << 20
+    cfg = (PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=4, k_d=2))
+           if algo == "gmm" else
+           PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=4), seed=17))
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    with _engine(cfg, w, h) as eng:
+        for t in range(n):
+            f = synth.make_frame("T", w, h, 31, t)
+            want = ref.process_frame(f)
+            if t == 9:
+                got = eng.process_frame(torch.from_numpy(f).cuda()).cpu().numpy()
+            else:
+                got = eng.process_frame(f)
+            np.testing.assert_array_equal(got, want, err_msg=f"frame {t}")
+        st = {k: v for k, v in eng.state_arrays().items()}
+    _assert_state_equal(st, ref.state_arrays(), list(st))
