@@ -250,6 +250,10 @@ struct HostStaging {
         crew = nullptr;
         if (crew_hold.owns_lock()) crew_hold.unlock();
     }
+    struct CrewRelease {  // drops the crew when a staging call returns, however it returns
+        HostStaging* h;
+        ~CrewRelease() { h->drop_crew(); }
+    };
 
     int ensure(int64_t ib, int64_t ob) {
         if (pin_in) return RGBDSEG_OK;
@@ -320,6 +324,7 @@ struct HostStaging {
             // and async calls never touch them
             const int64_t ch = ((in_bytes + IN_CHUNKS - 1) / IN_CHUNKS + 4095) / 4096 * 4096;  // >= 4096
             const bool helpers = in_bytes >= CREW_MIN_BYTES && ensure_crew();
+            CrewRelease release_on_exit{this};  // error returns included
             if (helpers) crew->post(in, pin_in, ch, in_bytes);
             int c = 0;
             for (int64_t off = 0; off < in_bytes; off += ch, ++c) {
@@ -388,6 +393,7 @@ struct HostStaging {
             memcpy(out + r0 * out_row, pin_out + r0 * out_row, (size_t)((r1 - r0) * out_row));
         };
         const bool helpers = ensure_crew();
+        CrewRelease release_on_exit{this};  // error returns included
         if (helpers) crew->post(in, pin_in, ch * in_row, rows * in_row);
         for (int64_t r0 = 0; r0 < rows; r0 += ch, ++n) {
             // masks of finished chunks leave while later chunks still upload
