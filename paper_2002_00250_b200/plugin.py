@@ -23,14 +23,16 @@ frame in one launch, so:
     current frame (GMM: calls carry no frame index) or when the frame index
     changes (PBAS); empty bands (more workers than rows) are harmless.
 
-`arrays()` is a live mapping in the reference layout, as the reference's
-(tests/test_acceptance.py:125-139 reads it after every frame).  Errors are
-the reference's exception classes (errors.py).
+`arrays()` is a live mapping in the reference layout from construction on,
+as the reference's (tests/test_acceptance.py:125-139 takes it before the
+first frame and reads it after every frame).  Errors are the reference's
+exception classes (errors.py).
 """
 
 from __future__ import annotations
 
 import threading
+from collections.abc import Mapping
 
 import numpy as np
 
@@ -52,25 +54,64 @@ class _Covered:
         return any(y0 < b1 and b0 < y1 for b0, b1 in self.ranges)
 
 
+class _LiveArrays(Mapping):
+    """arrays(): always reads the owner's current device state (the handle may
+    be re-created before the first frame, when the first band call brings
+    the depth mode / seed the constructor does not see)."""
+
+    def __init__(self, owner):
+        self._owner = owner
+
+    def _view(self):
+        return self._owner._current().state_arrays()
+
+    def __getitem__(self, key):
+        return self._view()[key]
+
+    def __iter__(self):
+        return iter(self._view())
+
+    def __len__(self):
+        return len(self._view())
+
+
 class _DeviceState:
     def __init__(self, width: int, height: int, device=None):
         self.width, self.height = int(width), int(height)
         self.device = device
         self.engine = None
+        self._cfg = None
+        self._frames = 0  # frames segmented by the current handle
         self._lock = threading.Lock()
         self._cov = _Covered(height)
 
+    def _default_config(self) -> PipelineConfig:
+        raise NotImplementedError
+
     def _ensure(self, cfg: PipelineConfig):
+        """The handle for `cfg`; before the first frame a handle created for
+        another depth mode / seed (state still initial) is replaced."""
         from .engine import SegmentationEngine
 
+        key = (cfg.mode, cfg.seed)
+        if self.engine is not None and self._cfg != key:
+            if self._frames:
+                raise ConfigError("the depth mode / seed changed after the first frame")
+            self.engine.close()
+            self.engine = None
         if self.engine is None:
             self.engine = SegmentationEngine(cfg, self.width, self.height, device=self.device)
+            self._cfg = key
         return self.engine
 
+    def _current(self):
+        with self._lock:
+            return self.engine if self.engine is not None else self._ensure(self._default_config())
+
     def arrays(self):
-        if self.engine is None:
-            raise ConfigError("the device state exists after the first segment_rows call")
-        return self.engine.state_arrays()
+        """Live mapping in the reference layout (gmm.py:251-255 / pbas.py:296-303),
+        valid from construction on, as the reference's."""
+        return _LiveArrays(self)
 
     def close(self) -> None:
         if self.engine is not None:
@@ -106,7 +147,11 @@ class GmmStateB200(_DeviceState):
                                               mode="rgbd" if use_depth else "rgb_only",
                                               gmm=self.params))
             np.copyto(mask, eng.process_frame(frame))
+            self._frames += 1
             self._cov.ranges = [(y0, y1)]
+
+    def _default_config(self) -> PipelineConfig:
+        return PipelineConfig(algorithm="gmm", mode="rgbd", gmm=self.params)
 
 
 class PbasStateB200(_DeviceState):
@@ -131,7 +176,7 @@ class PbasStateB200(_DeviceState):
             if self._frame == int(frame_idx) and not self._cov.overlaps(y0, y1):
                 self._cov.ranges.append((y0, y1))
                 return 0
-            if self._seed is not None and int(seed) != self._seed:
+            if self._frames and int(seed) != self._seed:
                 raise ConfigError("the seed changed between frames of one PbasState")
             self._seed = int(seed)
             eng = self._ensure(PipelineConfig(algorithm="pbas",
@@ -140,9 +185,13 @@ class PbasStateB200(_DeviceState):
             if eng.frame_idx != int(frame_idx):  # the caller's frame index is authoritative
                 eng.frame_idx = int(frame_idx)
             np.copyto(mask, eng.process_frame(frame))
+            self._frames += 1
             self._frame = int(frame_idx)
             self._cov.ranges = [(y0, y1)]
             return 0
+
+    def _default_config(self) -> PipelineConfig:
+        return PipelineConfig(algorithm="pbas", mode="rgbd", pbas=self.params, seed=0)
 
     def apply_intents(self, frame: np.ndarray, intents: np.ndarray, count: int,
                       use_depth: bool) -> None:

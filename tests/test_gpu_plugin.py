@@ -81,13 +81,17 @@ def test_plugin_states_under_the_reference_engine_loop(oracle_mod, algorithm, wo
     frames = synth.sequence("T" if algorithm == "pbas" else "S", w, h, seed=3, frames=30, k_rgb=5)
     ref = oracle_mod.OracleEngine(cfg, w, h, workers=workers)
     eng = ReferenceEngineLoop(cfg, w, h)
+    keys = gu.GMM_KEYS if algorithm == "gmm" else gu.PBAS_KEYS
+    # taken before the first frame, read after later ones (a live mapping, as
+    # GmmState/PbasState.arrays(); tests/test_acceptance.py:125-139 does this)
+    live = eng.state_arrays()
+    for k in keys:
+        np.testing.assert_array_equal(live[k], ref.state_arrays()[k], err_msg=f"{k} initial")
     try:
         for t, f in enumerate(frames):
             np.testing.assert_array_equal(eng.process_frame(f), ref.process_frame(f),
                                           err_msg=f"frame {t}")
             if t in (0, 12, 29):
-                live = eng.state_arrays()  # a live mapping, as GmmState/PbasState.arrays()
-                keys = gu.GMM_KEYS if algorithm == "gmm" else gu.PBAS_KEYS
                 for k in keys:
                     np.testing.assert_array_equal(live[k], ref.state_arrays()[k],
                                                   err_msg=f"{k} after frame {t}")
@@ -108,4 +112,13 @@ def test_plugin_pbas_never_hands_out_intents():
         st.apply_intents(frame, None, 3, True)
     with pytest.raises(ConfigError):  # one PbasState, one seed (engine.py:127)
         st.segment_rows(frame, 1, 0, 4, True, np.uint64(2), mask, None)
+    st.close()
+    # arrays() before the first frame, then a first frame with another seed:
+    # the initial handle is replaced and the mapping follows it
+    st = PbasStateB200(8, 4, PbasParams(n=4), device=0)
+    arr = st.arrays()
+    assert int(arr["len_rgb"].max()) == 0
+    for t in range(6):
+        st.segment_rows(frame, t, 0, 4, True, np.uint64(77), mask, None)
+    assert int(arr["len_rgb"].max()) == 2  # 6 frames, n = 4: two dmin pushes
     st.close()
