@@ -598,6 +598,18 @@ def run_ours(args, rank, world, local_rank):
             traffic = json.loads(tfile.read_text()).get(f"{tkey}:{args.workload}")
         except Exception:
             traffic = None
+    # PBAS's measured bytes per launch at the steady state the bench times
+    # (strip K2 + K3 list, ncu), beside its algorithmic bytes
+    if "pbas" in per_algo and tfile.exists() and not args.pbas_gradient:
+        try:
+            tj = json.loads(tfile.read_text())
+            k2, k3 = tj.get(f"pbas:{args.workload}"), tj.get(f"pbas_apply:{args.workload}")
+            if k2 is not None and k3 is not None:
+                per_algo["pbas"]["traffic_per_step_ncu"] = k2 + k3
+                per_algo["pbas"]["traffic_frac_of_peak"] = (
+                    (k2 + k3) / (per_algo["pbas"]["ms_per_step"] / 1e3) / 1e9 / peak)
+        except Exception:
+            pass
     roof = {"bound": "hbm", "achieved": per_algo[dom].get("achieved_gbs"), "peak": peak,
             "unit": "GB/s", "frac": per_algo[dom].get("roofline_frac"), "traffic": traffic,
             "kernel": (f"gmm_step_kernel<{gmm_k[0]},{gmm_k[1]},{'StF32' if args.gmm_state == 'f32' else 'StF64'}> (K1)"
