@@ -191,3 +191,37 @@ def test_gmm_1080p_regime_s_50_frames_vs_oracle(oracle_mod):
             assert d == 0, f"frame {t}: {d} mask pixels differ"
         _assert_state_equal(eng.state_arrays(), ref.state_arrays(), gu.GMM_KEYS, "GMM 1080p")
     assert (ref.state_arrays()["rgb_w"] > 0).all()  # regime S seeds every component
+
+
+def test_pbas_1080p_steady_state_strips_vs_oracle(oracle_mod):
+    # The bench's steady state at full size: one 1920x1080 stream of regime T
+    # cycling through an 8-frame ring as bench.py does (repeating noise ages
+    # T to t_lower within ~300 frames; fresh noise every frame takes >1000,
+    # see the config-3 test), 400 frames, K2 in auto mode
+    # (rows while young, then the staged warp-strip kernel; device frames, so
+    # no host-path chunking) -- masks every 20th frame and every frame after
+    # 380, full state at the end, bit-exact with the oracle.
+    import torch
+
+    from paper_2002_00250_b200 import _native
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    w, h, n = 1920, 1080, 400
+    cfg = PipelineConfig(algorithm="pbas", mode="rgbd", pbas=PbasParams(n=20), seed=3)
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    L = _native.lib()
+    modes = []
+    with SegmentationEngine(cfg, w, h, device=0) as eng:
+        ring = [synth.make_frame("T", w, h, 2, k) for k in range(8)]
+        ring_dev = [torch.from_numpy(f).cuda() for f in ring]
+        for t in range(n):
+            f = ring[t % 8]
+            got = eng.process_frame(ring_dev[t % 8])
+            want = ref.process_frame(f)
+            modes.append(int(L.rgbdseg_pbas_get_k2_mode(eng._h.ptr)))
+            if t % 20 == 0 or t >= 380:
+                np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"frame {t}")
+        _assert_state_equal(eng.state_arrays(), ref.state_arrays(), gu.PBAS_KEYS, "after 400")
+    t_final = ref.state_arrays()["t"]
+    assert float(np.mean(t_final == cfg.pbas.t_lower)) > 0.9
+    assert modes[25] == 1 and modes[-1] == 2, (modes[25], modes[-1])
