@@ -1,12 +1,10 @@
 #!/bin/bash
-# f32 GMM storage: GPU tests, bench A/B (f64 default vs --gmm-state f32), one ncu capture.
+# Opt-in f32 GMM storage: K1 occupancy variants (tuning/lib_f*.so), config 4.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-mkdir -p gpurun_out
-export PYTHONUNBUFFERED=1
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout 900 python -m pytest tests/test_gmm_f32.py tests/test_gpu_parity.py -m gpu -q -x -k "gmm or f32 or golden" > gpurun_out/pytest_f32.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_f32.log
-timeout 300 python bench.py --steps 100 --warmup 10 --no-cpu-baseline > gpurun_out/bench_f64.json 2> gpurun_out/bench_f64.err
-timeout 300 python bench.py --steps 100 --warmup 10 --no-cpu-baseline --gmm-state f32 > gpurun_out/bench_f32.json 2> gpurun_out/bench_f32.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gmm_step -s 44 -c 1 \
-    -o gpurun_out/full_f32_gmm python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --gmm-state f32 > gpurun_out/full_f32_gmm.log 2>&1
-echo done
+export RGBDSEG_B200_AUTOBUILD=0
+for lib in "" tuning/lib_f*.so; do
+  tag=${lib:-default}; tag=$(basename "$tag" .so)
+  RGBDSEG_B200_LIB=${lib:+$PWD/$lib} timeout 300 python bench.py --gmm-state f32 --steps 50 --warmup 5 --no-e2e \
+    --no-cpu-baseline --no-verify > gpurun_out/f32.json 2>/dev/null
+  echo "$tag $(python -c "import json;d=json.load(open('gpurun_out/f32.json'));p=d['per_algo']['gmm'];print(round(p['ms_per_step'],4),'ms', round(p['roofline_frac'],3), round(d['ms_per_step'],4))")"
+done
