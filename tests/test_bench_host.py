@@ -51,3 +51,22 @@ def test_b_alg_table_matches_survey():
     assert bench.B_ALG[("gmm_f32", 7, 3)] == 245
     # f32: half of the 352 + 128 state bytes + 5 frame/mask bytes; 3/3: (192 + 96) / 2 + 5
     assert bench.B_ALG[("gmm_f32", 3, 3)] == (192 + 96) // 2 + 5
+
+
+def test_bit_equality_folds_are_position_weighted_and_match_torch():
+    # bench._fold_np / _fold_dev: position-weighted 64-bit folds (wrapping),
+    # the cross-rank bit-equality proof of config 5 and the stream digests
+    import numpy as np
+    import torch
+
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 256, size=1003, dtype=np.uint8)
+    words = np.concatenate([a, np.zeros((-a.size) % 8, np.uint8)]).view(np.uint64)
+    want = sum(int(w) * (2 * i + 1) for i, w in enumerate(words)) % (1 << 64)
+    assert bench._fold_np(a) == want
+    # torch's int64 fold is the same number modulo 2^64
+    assert bench._fold_dev(torch.from_numpy(a)) % (1 << 64) == want
+    b = a.copy()
+    b[[0, 8]] = b[[8, 0]]  # same bytes, different positions
+    assert bench._fold_np(b) != bench._fold_np(a) or a[0] == a[8]
+    assert bench._mix(bench._mix(0, 1), 2) != bench._mix(bench._mix(0, 2), 1)
