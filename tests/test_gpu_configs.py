@@ -225,3 +225,42 @@ def test_pbas_1080p_steady_state_strips_vs_oracle(oracle_mod):
     t_final = ref.state_arrays()["t"]
     assert float(np.mean(t_final == cfg.pbas.t_lower)) > 0.9
     assert modes[25] == 1 and modes[-1] == 2, (modes[25], modes[-1])
+
+
+def test_gmm_1080p_regime_t_scene_change_vs_oracle(oracle_mod):
+    # GMM 7/3 trained on regime S, then fed regime T at 1080p: every pixel is
+    # unmatched at first (least-fit replacement with the FP32 argmin estimate
+    # and its FP64 fallback, gmm.py:326-337), then the moving objects keep
+    # replacing -- masks and state bit-exact with the oracle.
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    w, h = 1920, 1080
+    cfg = PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=7, k_d=3))
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    with SegmentationEngine(cfg, w, h, device=0) as eng:
+        seq = [("S", t) for t in range(8)] + [("T", t) for t in range(20)]
+        for i, (regime, t) in enumerate(seq):
+            f = synth.make_frame(regime, w, h, 6, t)
+            d = int(np.count_nonzero(eng.process_frame(f) != ref.process_frame(f)))
+            assert d == 0, f"frame {i} ({regime}{t}): {d} mask pixels differ"
+        _assert_state_equal(eng.state_arrays(), ref.state_arrays(), gu.GMM_KEYS, "scene change")
+
+
+def test_pbas_1080p_rgb_only_strips_vs_oracle(oracle_mod):
+    # rgb_only PBAS (no depth group) through the pinned strip kernel at 1080p
+    import torch
+
+    from paper_2002_00250_b200 import _native
+    from paper_2002_00250_b200.engine import SegmentationEngine
+
+    w, h = 1920, 1080
+    cfg = PipelineConfig(algorithm="pbas", mode="rgb_only", pbas=PbasParams(n=20, t_dec=1.0),
+                         seed=4)
+    ref = oracle_mod.OracleEngine(cfg, w, h, workers=oracle_mod.cpu_threads())
+    with SegmentationEngine(cfg, w, h, device=0) as eng:
+        _native.check(_native.lib().rgbdseg_pbas_set_k2_mode(eng._h.ptr, 2))
+        for t in range(40):
+            f = synth.make_frame("T", w, h, 8, t % 8)
+            got = eng.process_frame(torch.from_numpy(f).cuda()).cpu().numpy()
+            np.testing.assert_array_equal(got, ref.process_frame(f), err_msg=f"frame {t}")
+        _assert_state_equal(eng.state_arrays(), ref.state_arrays(), gu.PBAS_KEYS, "rgb_only")
