@@ -171,12 +171,18 @@ struct CopyCrew {
             if (quit.load()) return;
             seen = gen.load(std::memory_order_acquire);
             const uint64_t tag = seen << 32;
-            for (int c = 0; c < nchunks; ++c) {
-                const int64_t off = c * chunk, n = total - off < chunk ? total - off : chunk;
+            // the job's fields, read once: the next post() may rewrite them as
+            // soon as this job's last chunk is reported
+            const uint8_t* const js = src;
+            uint8_t* const jd = dst;
+            const int64_t jc = chunk, jt = total;
+            const int jn = nchunks;
+            for (int c = 0; c < jn; ++c) {
+                const int64_t off = c * jc, n = jt - off < jc ? jt - off : jc;
                 const int64_t half = (n / NT + 63) / 64 * 64;
                 const int64_t o = off + t * half;
                 const int64_t m = o >= off + n ? 0 : (off + n - o < half || t == NT - 1 ? off + n - o : half);
-                if (m > 0) memcpy(dst + o, src + o, (size_t)m);
+                if (m > 0) memcpy(jd + o, js + o, (size_t)m);
                 done[t].store(tag | (uint64_t)(c + 1), std::memory_order_release);
             }
         }
@@ -255,8 +261,18 @@ struct HostStaging {
         ~CrewRelease() { h->drop_crew(); }
     };
 
+    bool ready = false;  // every buffer, event and stream below exists
+
     int ensure(int64_t ib, int64_t ob) {
-        if (pin_in) return RGBDSEG_OK;
+        if (ready) return RGBDSEG_OK;
+        if (int rc = allocate(ib, ob)) {
+            release();  // a partial allocation is not kept
+            return rc;
+        }
+        ready = true;
+        return RGBDSEG_OK;
+    }
+    int allocate(int64_t ib, int64_t ob) {
         in_bytes = ib;
         out_bytes = ob;
         RGBDSEG_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&pin_in), ib, cudaHostAllocDefault));
