@@ -210,3 +210,13 @@ def test_gpu_f32_match_gate_band_exact(oracle_mod):
                                   gmm=GmmParams(k_rgb=3, k_d=2, var_init=4.0, match_lambda=2.5,
                                                 alpha=0.25)))
         _gpu_vs_f32_oracle(oracle_mod, cfg, frames)
+
+
+@pytest.mark.gpu
+def test_gpu_f32_1080p_row_chunked_host_path(oracle_mod):
+    # process_frame(numpy) at 1080p runs the row-chunked staged host path
+    # (K1 per row chunk); with f32 storage the state stays bit-exact with the
+    # round-on-store f32 oracle, masks within the north_star floor.
+    frames = [synth.make_frame("S", 1920, 1080, 3, t) for t in range(10)]
+    cfg = _f32(PipelineConfig(algorithm="gmm", mode="rgbd", gmm=GmmParams(k_rgb=7, k_d=3)))
+    _gpu_vs_f32_oracle(oracle_mod, cfg, frames)
